@@ -1,0 +1,110 @@
+/*
+ * libutvb200 — C ABI of the B200-native powerURV / randUTV hot path.
+ *
+ * The reference (utvkit, arXiv 2106.13402) has no FFI layer: its boundary is
+ * the Python API re-exported by utvkit/__init__.py.  Each entry point below
+ * replaces one reference function on that path (file:line cited); the
+ * Python package paper_2106_13402_b200 binds them with ctypes and keeps the
+ * reference's signatures, result types and exceptions.
+ *
+ * Conventions
+ *  - All matrices are column-major FP64 device pointers with an explicit
+ *    leading dimension.  Leading dimensions must be EVEN (TMA stride rule);
+ *    pointers must be 8-byte aligned.
+ *  - `work` is a caller-allocated device workspace of `lwork` bytes; query
+ *    the size with the matching *_bufsize function.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  No entry
+ *    point synchronises the host; results are ready when the stream is.
+ *  - Return value: 0 ok; -i = argument i is invalid (LAPACK `info` style);
+ *    -1000 CUDA error; -1001 workspace too small; -1002 alignment;
+ *    > 0 numerical failure reported through a device status word.
+ *  - Deterministic: identical inputs give bitwise identical outputs.
+ */
+#ifndef UTV_B200_H
+#define UTV_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Library/ABI version (major*100 + minor). */
+int utv_version(void);
+
+/* Number of SMs of the current device (0 if no device). */
+int utv_device_sms(void);
+
+/* C = alpha*op(A)*op(B) + beta*C ; op = 'N' | 'T'.
+ * Replaces numpy `@` on the hot path (randutv.py:190-192, qr.py:116,120,131,
+ * powerurv.py:64,66, randutv.py:152-156).  FP64 DMMA tensor cores, TMA. */
+size_t utv_dgemm_bufsize(int m, int n, int k);
+int utv_dgemm(char transa, char transb, int m, int n, int k, double alpha, const double* A,
+              long lda, const double* B, long ldb, double beta, double* C, long ldc, void* work,
+              size_t lwork, void* stream);
+
+/* Sum of squares of an m x n block -> *out (device scalar).
+ * Replaces frobenius_norm (matrix.py:79-81) and ErrorTracker.update's panel
+ * mass (randutv.py:52-62). */
+size_t utv_dsumsq_bufsize(void);
+int utv_dsumsq(int m, int n, const double* A, long lda, double* out, void* work, size_t lwork,
+               void* stream);
+
+/* Householder QR, m >= n: A <- R (zeros below the diagonal), Y (m x n unit
+ * lower trapezoidal, zeros above), T (n x n upper, forward compact WY).
+ * Replaces hqr_full (qr.py:71-100) incl. _reflector (qr.py:43-60) and
+ * _append_twy_column (qr.py:63-68); skip rule and sign convention kept. */
+size_t utv_dgeqrf_bufsize(int m, int n);
+int utv_dgeqrf(int m, int n, double* A, long lda, double* Y, long ldy, double* T, long ldt,
+               void* work, size_t lwork, void* stream);
+
+/* Apply Q = I - Y T Y^T (k x k, w reflectors) to the m x n block B:
+ * side 'L': B <- Q B or Q^T B (trans 'N'/'T'), requires m == k;
+ * side 'R': B <- B Q or B Q^T, requires n == k.
+ * Replaces apply_q (qr.py:103-121). */
+size_t utv_dlarfb_bufsize(int m, int n, int w);
+int utv_dlarfb(char side, char trans, int m, int n, int k, int w, const double* Y, long ldy,
+               const double* T, long ldt, double* B, long ldb, void* work, size_t lwork,
+               void* stream);
+
+/* Q[:, :ncols] = I - Y (T Y[:ncols, :]^T), Y is m x w.
+ * Replaces materialize_q (qr.py:124-131) / hqr_thin's Q (qr.py:134-138). */
+size_t utv_dorgqr_bufsize(int m, int ncols, int w);
+int utv_dorgqr(int m, int ncols, int w, const double* Y, long ldy, const double* T, long ldt,
+               double* Q, long ldq, void* work, size_t lwork, void* stream);
+
+/* SVD of an n x n block by one-sided Jacobi: sigma descending, full U, V,
+ * reference sign rule.  *status (device int) = sweeps used, -1 = no
+ * convergence.  Replaces svd_dense(a, "full") (svd.py:37-58). n <= 400. */
+size_t utv_dgesvj_bufsize(int n);
+int utv_dgesvj(int n, const double* A, long lda, double* sigma, double* U, long ldu, double* V,
+               long ldv, int* status, void* work, size_t lwork, void* stream);
+
+/* Blocked randUTV, basic variant (randutv_basic, randutv.py:228-235 ->
+ * _randutv 110-182, _sample_basic 185-193).
+ *  T (m x n): on entry A, on exit T.   U (m x m), V (n x n): on entry I.
+ *  G: the reference's Gaussian draws; block i (k_i = m - i*b rows) is the
+ *     C-order k_i x b draw, i.e. a b x k_i column-major matrix with leading
+ *     dimension ldg (>= b, even), stored at column offset sum_{i'<i} k_i'.
+ *  errsq[i]  (device, ceil(n/b)): ||T[lo:mid, lo:]||_F^2 after step i.
+ *  trail2[i] (device or NULL):    ||T[mid:, mid:]||_F^2 after step i.
+ *  svd_status[i] (device int): Jacobi sweeps of step i (-1 = no convergence). */
+size_t utv_randutv_basic_bufsize(int m, int n, int b, int q);
+int utv_randutv_basic_f64(int m, int n, int b, int q, double* T, long ldt, double* U, long ldu,
+                          double* V, long ldv, const double* G, long ldg, double* errsq,
+                          double* trail2, int* svd_status, void* work, size_t lwork,
+                          void* stream);
+
+/* powerURV (power_urv_from_sample, powerurv.py:41-72; power_urv :75-79;
+ * rurv :82-84 with q = 0).  A (m x n, read only), G (n x n, read only).
+ * Outputs Uq = (Uy m x n, Ut n x n), R (m x n), Vq = (Vy n x n, Vt n x n). */
+size_t utv_powerurv_bufsize(int m, int n, int q);
+int utv_powerurv_f64(int m, int n, int q, const double* A, long lda, const double* G, long ldg,
+                     double* Uy, long lduy, double* Ut, long ldut, double* R, long ldr,
+                     double* Vy, long ldvy, double* Vt, long ldvt, void* work, size_t lwork,
+                     void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UTV_B200_H */

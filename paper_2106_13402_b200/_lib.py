@@ -1,0 +1,158 @@
+"""ctypes binding of libutvb200.so (include/utv_b200.h) + device-matrix helpers.
+
+PyTorch is used only for device memory, streams and host<->device copies.
+There is no CPU fallback: if the library or a CUDA device is missing every
+compute entry point raises ``RuntimeError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libutvb200.so")
+
+_lib = None
+
+c_int, c_long, c_double, c_size_t, c_void_p, c_char = (
+    ctypes.c_int, ctypes.c_long, ctypes.c_double, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_char)
+
+# name -> (restype, argtypes)
+SIGNATURES = {
+    "utv_version": (c_int, []),
+    "utv_device_sms": (c_int, []),
+    "utv_dgemm_bufsize": (c_size_t, [c_int, c_int, c_int]),
+    "utv_dgemm": (c_int, [c_char, c_char, c_int, c_int, c_int, c_double, c_void_p, c_long,
+                          c_void_p, c_long, c_double, c_void_p, c_long, c_void_p, c_size_t, c_void_p]),
+    "utv_dsumsq_bufsize": (c_size_t, []),
+    "utv_dsumsq": (c_int, [c_int, c_int, c_void_p, c_long, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "utv_dgeqrf_bufsize": (c_size_t, [c_int, c_int]),
+    "utv_dgeqrf": (c_int, [c_int, c_int, c_void_p, c_long, c_void_p, c_long, c_void_p, c_long,
+                           c_void_p, c_size_t, c_void_p]),
+    "utv_dlarfb_bufsize": (c_size_t, [c_int, c_int, c_int]),
+    "utv_dlarfb": (c_int, [c_char, c_char, c_int, c_int, c_int, c_int, c_void_p, c_long, c_void_p,
+                           c_long, c_void_p, c_long, c_void_p, c_size_t, c_void_p]),
+    "utv_dorgqr_bufsize": (c_size_t, [c_int, c_int, c_int]),
+    "utv_dorgqr": (c_int, [c_int, c_int, c_int, c_void_p, c_long, c_void_p, c_long, c_void_p,
+                           c_long, c_void_p, c_size_t, c_void_p]),
+    "utv_dgesvj_bufsize": (c_size_t, [c_int]),
+    "utv_dgesvj": (c_int, [c_int, c_void_p, c_long, c_void_p, c_void_p, c_long, c_void_p, c_long,
+                           c_void_p, c_void_p, c_size_t, c_void_p]),
+    "utv_randutv_basic_bufsize": (c_size_t, [c_int, c_int, c_int, c_int]),
+    "utv_randutv_basic_f64": (c_int, [c_int, c_int, c_int, c_int, c_void_p, c_long, c_void_p,
+                                      c_long, c_void_p, c_long, c_void_p, c_long, c_void_p,
+                                      c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "utv_powerurv_bufsize": (c_size_t, [c_int, c_int, c_int]),
+    "utv_powerurv_f64": (c_int, [c_int, c_int, c_int, c_void_p, c_long, c_void_p, c_long,
+                                 c_void_p, c_long, c_void_p, c_long, c_void_p, c_long, c_void_p,
+                                 c_long, c_void_p, c_long, c_void_p, c_size_t, c_void_p]),
+}
+
+
+def load():
+    """Load libutvb200.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"libutvb200.so not found at {LIB_PATH}; build it with "
+                "`python -m paper_2106_13402_b200.build` (no CPU fallback exists)")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+class UtvError(RuntimeError):
+    pass
+
+
+def check(status, what):
+    if status != 0:
+        raise UtvError(f"{what} failed with status {status}")
+
+
+# ---------------------------------------------------------------------------
+# device matrices
+# ---------------------------------------------------------------------------
+
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2106_13402_b200 needs a CUDA device (B200); no CPU fallback")
+    return torch
+
+
+def even_ld(rows):
+    return max(2, rows + (rows & 1))
+
+
+@dataclass
+class DMat:
+    """Column-major FP64 device matrix backed by a torch tensor of shape (cols, ld)."""
+    t: object
+    rows: int
+    cols: int
+    ld: int
+
+    @property
+    def ptr(self):
+        return self.t.data_ptr()
+
+    def at(self, r, c):
+        return self.t.data_ptr() + 8 * (r + c * self.ld)
+
+    def to_numpy(self):
+        host = self.t[:, :self.rows].cpu().numpy()      # (cols, rows) C order
+        return host.T                                   # (rows, cols) F order
+
+
+def dempty(rows, cols, ld=None):
+    torch = torch_cuda()
+    ld = even_ld(rows) if ld is None else ld
+    t = torch.empty((max(cols, 1), ld), dtype=torch.float64, device="cuda")
+    return DMat(t, rows, cols, ld)
+
+
+def dzeros(rows, cols):
+    m = dempty(rows, cols)
+    m.t.zero_()
+    return m
+
+
+def deye(n):
+    torch = torch_cuda()
+    m = dzeros(n, n)
+    idx = torch.arange(n, device="cuda")
+    m.t[idx, idx] = 1.0
+    return m
+
+
+def dfrom_numpy(a, pinned=False):
+    """Copy a 2-D float64 array to the device (column-major, even ld)."""
+    torch = torch_cuda()
+    a = np.asfortranarray(a, dtype=np.float64)
+    rows, cols = a.shape
+    m = dempty(rows, cols)
+    src = torch.from_numpy(a.T)             # (cols, rows) view of the F-order data
+    if pinned:
+        src = src.pin_memory()
+    m.t[:cols, :rows].copy_(src, non_blocking=pinned)
+    return m
+
+
+def workspace(nbytes):
+    torch = torch_cuda()
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device="cuda")
+
+
+def stream_ptr():
+    torch = torch_cuda()
+    return torch.cuda.current_stream().cuda_stream

@@ -1,0 +1,163 @@
+// extern "C" entry points of libutvb200 (declared in include/utv_b200.h).
+// No C++ exception crosses this boundary; every function returns a status.
+#include "../../include/utv_b200.h"
+#include "common.cuh"
+#include "utv_internal.h"
+
+namespace utv {
+size_t randutv_ws_doubles(int m, int n, int b);
+int randutv_basic(int m, int n, int b, int q, Mat T, Mat U, Mat V, const double* G, long ldg,
+                  double* errsq, double* trail2, int* svd_status, double* ws, size_t ws_doubles,
+                  cudaStream_t st);
+size_t powerurv_ws_doubles(int m, int n);
+int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, Mat Vt, double* ws,
+             size_t ws_doubles, cudaStream_t st);
+}  // namespace utv
+
+using namespace utv;
+
+static inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
+static inline size_t B(size_t doubles) { return doubles * sizeof(double) + 4096; }
+static inline bool ld_ok(long ld, int rows) { return ld >= (rows > 1 ? rows : 1) && (ld & 1) == 0; }
+
+extern "C" {
+
+int utv_version(void) { return 100; }
+
+int utv_device_sms(void) {
+  int n = 0, dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  return n;
+}
+
+size_t utv_dgemm_bufsize(int, int, int) { return B(SPLITK_WS); }
+
+int utv_dgemm(char transa, char transb, int m, int n, int k, double alpha, const double* A,
+              long lda, const double* Bm, long ldb, double beta, double* C, long ldc, void* work,
+              size_t lwork, void* stream) {
+  const bool ta = (transa == 'T' || transa == 't'), tb = (transb == 'T' || transb == 't');
+  if (!ta && transa != 'N' && transa != 'n') return -1;
+  if (!tb && transb != 'N' && transb != 'n') return -2;
+  if (m < 0) return -3;
+  if (n < 0) return -4;
+  if (k < 0) return -5;
+  if (k > 0 && !ld_ok(lda, ta ? k : m)) return -8;
+  if (k > 0 && !ld_ok(ldb, tb ? n : k)) return -10;
+  if (!ld_ok(ldc, m)) return -13;
+  return dgemm(ta, tb, m, n, k, alpha, A, lda, Bm, ldb, beta, C, ldc, (double*)work,
+               work ? lwork / sizeof(double) : 0, S(stream));
+}
+
+size_t utv_dsumsq_bufsize(void) { return B(sumsq_scratch_doubles()); }
+
+int utv_dsumsq(int m, int n, const double* A, long lda, double* out, void* work, size_t lwork,
+               void* stream) {
+  if (m < 0) return -1;
+  if (n < 0) return -2;
+  if (lwork < sumsq_scratch_doubles() * sizeof(double)) return UTV_ERR_WORKSPACE;
+  return sumsq(A, lda, m, n, out, (double*)work, S(stream));
+}
+
+size_t utv_dgeqrf_bufsize(int m, int n) { return B(geqrf_ws_doubles(m, n, true)); }
+
+int utv_dgeqrf(int m, int n, double* A, long lda, double* Y, long ldy, double* T, long ldt,
+               void* work, size_t lwork, void* stream) {
+  if (m < 1) return -1;
+  if (n < 1 || n > m) return -2;
+  if (!ld_ok(lda, m)) return -4;
+  if (!ld_ok(ldy, m)) return -6;
+  if (!ld_ok(ldt, n)) return -8;
+  return geqrf(Mat{A, lda, m, n}, Mat{Y, ldy, m, n}, Mat{T, ldt, n, n}, true, (double*)work,
+               lwork / sizeof(double), S(stream));
+}
+
+size_t utv_dlarfb_bufsize(int m, int n, int w) { return B(larfb_ws_doubles(m, n, w)); }
+
+int utv_dlarfb(char side, char trans, int m, int n, int k, int w, const double* Y, long ldy,
+               const double* T, long ldt, double* Bm, long ldb, void* work, size_t lwork,
+               void* stream) {
+  const bool left = (side == 'L' || side == 'l');
+  if (!left && side != 'R' && side != 'r') return -1;
+  const bool tr = (trans == 'T' || trans == 't');
+  if (!tr && trans != 'N' && trans != 'n') return -2;
+  if (m < 0) return -3;
+  if (n < 0) return -4;
+  if (k < 1 || (left ? m != k : n != k)) return -5;
+  if (w < 1 || w > k) return -6;
+  if (!ld_ok(ldy, k)) return -8;
+  if (!ld_ok(ldt, w)) return -10;
+  if (!ld_ok(ldb, m)) return -12;
+  return larfb(left ? 'L' : 'R', tr, Mat{(double*)Y, ldy, k, w}, Mat{(double*)T, ldt, w, w},
+               Mat{Bm, ldb, m, n}, (double*)work, lwork / sizeof(double), S(stream));
+}
+
+size_t utv_dorgqr_bufsize(int m, int ncols, int w) {
+  return B((size_t)round_up(w, 4) * ncols + SPLITK_WS + 1024);
+}
+
+int utv_dorgqr(int m, int ncols, int w, const double* Y, long ldy, const double* T, long ldt,
+               double* Q, long ldq, void* work, size_t lwork, void* stream) {
+  if (m < 1) return -1;
+  if (ncols < 1 || ncols > m) return -2;
+  if (w < 1 || w > m) return -3;
+  if (!ld_ok(ldy, m)) return -5;
+  if (!ld_ok(ldt, w)) return -7;
+  if (!ld_ok(ldq, m)) return -9;
+  return orgqr(Mat{(double*)Y, ldy, m, w}, Mat{(double*)T, ldt, w, w}, Mat{Q, ldq, m, ncols},
+               (double*)work, lwork / sizeof(double), S(stream));
+}
+
+size_t utv_dgesvj_bufsize(int n) { return B(gesvj_ws_doubles(n)); }
+
+int utv_dgesvj(int n, const double* A, long lda, double* sigma, double* U, long ldu, double* V,
+               long ldv, int* status, void* work, size_t lwork, void* stream) {
+  if (n < 1 || n > 400) return -1;
+  if (lda < n) return -3;
+  if (ldu < n) return -6;
+  if (ldv < n) return -8;
+  return gesvj(Mat{(double*)A, lda, n, n}, sigma, Mat{U, ldu, n, n}, Mat{V, ldv, n, n},
+               (double*)work, lwork / sizeof(double), status, S(stream));
+}
+
+size_t utv_randutv_basic_bufsize(int m, int n, int b, int) { return B(randutv_ws_doubles(m, n, b)); }
+
+int utv_randutv_basic_f64(int m, int n, int b, int q, double* T, long ldt, double* U, long ldu,
+                          double* V, long ldv, const double* G, long ldg, double* errsq,
+                          double* trail2, int* svd_status, void* work, size_t lwork,
+                          void* stream) {
+  if (m < 1) return -1;
+  if (n < 1 || n > m) return -2;
+  if (b < 1 || b > 400) return -3;
+  if (q < 0) return -4;
+  if (!ld_ok(ldt, m)) return -6;
+  if (!ld_ok(ldu, m)) return -8;
+  if (!ld_ok(ldv, n)) return -10;
+  if (n > b && !ld_ok(ldg, b)) return -12;
+  return randutv_basic(m, n, b, q, Mat{T, ldt, m, n}, Mat{U, ldu, m, m}, Mat{V, ldv, n, n}, G, ldg,
+                       errsq, trail2, svd_status, (double*)work, lwork / sizeof(double),
+                       S(stream));
+}
+
+size_t utv_powerurv_bufsize(int m, int n, int) { return B(powerurv_ws_doubles(m, n)); }
+
+int utv_powerurv_f64(int m, int n, int q, const double* A, long lda, const double* G, long ldg,
+                     double* Uy, long lduy, double* Ut, long ldut, double* R, long ldr,
+                     double* Vy, long ldvy, double* Vt, long ldvt, void* work, size_t lwork,
+                     void* stream) {
+  if (m < 1) return -1;
+  if (n < 1 || n > m) return -2;
+  if (q < 0) return -3;
+  if (!ld_ok(lda, m)) return -5;
+  if (!ld_ok(ldg, n)) return -7;
+  if (!ld_ok(lduy, m)) return -9;
+  if (!ld_ok(ldut, n)) return -11;
+  if (!ld_ok(ldr, m)) return -13;
+  if (!ld_ok(ldvy, n)) return -15;
+  if (!ld_ok(ldvt, n)) return -17;
+  return powerurv(m, n, q, Mat{(double*)A, lda, m, n}, Mat{(double*)G, ldg, n, n},
+                  Mat{Uy, lduy, m, n}, Mat{Ut, ldut, n, n}, Mat{R, ldr, m, n}, Mat{Vy, ldvy, n, n},
+                  Mat{Vt, ldvt, n, n}, (double*)work, lwork / sizeof(double), S(stream));
+}
+
+}  // extern "C"

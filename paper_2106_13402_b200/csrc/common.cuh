@@ -1,0 +1,143 @@
+// Shared device/host helpers for libutvb200 (sm_100a only).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
+#error "libutvb200 is written for sm_100a only"
+#endif
+
+namespace utv {
+
+// Status codes of the C-ABI (include/utv_b200.h).
+enum : int {
+  UTV_OK = 0,
+  UTV_ERR_CUDA = -1000,      // a CUDA runtime call failed
+  UTV_ERR_WORKSPACE = -1001, // workspace too small
+  UTV_ERR_ALIGN = -1002,     // leading dimension not even / pointer not 8-byte aligned
+  UTV_ERR_NOCONV = 1,        // Jacobi SVD did not converge within the sweep cap
+};
+
+#define UTV_CUDA(call)                                                          \
+  do {                                                                          \
+    cudaError_t e_ = (call);                                                    \
+    if (e_ != cudaSuccess) {                                                    \
+      fprintf(stderr, "libutvb200: %s failed: %s (%s:%d)\n", #call,             \
+              cudaGetErrorString(e_), __FILE__, __LINE__);                      \
+      return UTV_ERR_CUDA;                                                      \
+    }                                                                           \
+  } while (0)
+
+#define UTV_CHECK(expr)                                                         \
+  do {                                                                          \
+    int s_ = (expr);                                                            \
+    if (s_ != 0) return s_;                                                     \
+  } while (0)
+
+inline int ceil_div(long a, long b) { return (int)((a + b - 1) / b); }
+inline long round_up(long a, long b) { return (a + b - 1) / b * b; }
+
+// Column-major matrix view (device pointer + leading dimension).
+struct Mat {
+  double* p;
+  long ld;
+  int rows, cols;
+  __host__ __device__ double* at(long r, long c) const { return p + r + c * ld; }
+  __host__ __device__ Mat sub(int r, int c, int nr, int nc) const {
+    return Mat{p + r + (long)c * ld, ld, nr, nc};
+  }
+};
+
+// Simple bump allocator over a caller-provided device workspace.
+struct Arena {
+  char* base;
+  size_t size;
+  size_t used;
+  double* take(size_t n_doubles) {
+    size_t bytes = round_up((long)(n_doubles * sizeof(double)), 256);
+    if (used + bytes > size) return nullptr;
+    double* p = (double*)(base + used);
+    used += bytes;
+    return p;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// PTX wrappers (mbarrier, TMA, DMMA)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)map) : "memory");
+}
+
+// D(8x8) += A(8x4, row) * B(4x8, col), FP64 tensor core (SASS DMMA.8x8x4).
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// Grid-wide barrier for cooperative launches: monotone counter, one arrival per CTA.
+__device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace utv

@@ -1,0 +1,407 @@
+// K1: FP64 GEMM on the B200 DMMA tensor pipe, operands staged by TMA.
+//
+//   C = alpha * op(A) * op(B) + beta * C      (column-major, op in {N, T})
+//
+// Replaces every numpy `@` on the hot path: sampling (randutv.py:190-192),
+// the three GEMMs of apply_q (qr.py:116,120), materialize_q (qr.py:131),
+// A*V / A^T*Vhat in powerURV (powerurv.py:64,66) and the small-SVD rotations
+// (randutv.py:152-156,167-172).
+//
+// Design (sm_100a):
+//  * CTA tile 128x128x16, 8 DMMA warps (2x4, warp tile 64x32, 252 regs);
+//    thread 0 also drives TMA through a STAGES-deep full/empty mbarrier ring
+//    of 128B-swizzled smem tiles.
+//  * mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4). tcgen05 has no f64 kind.
+//  * Fragment rows/cols are mapped onto the 128B-swizzled tiles with a
+//    permutation that makes every 64-bit fragment load bank-conflict free
+//    (see DESIGN.md "GEMM smem layout").
+//  * TMA zero-fills out-of-bounds boxes, so ragged M/N/K need no predication
+//    on the load side; sub-matrix pointers that are not 16B aligned are
+//    handled by shifting the tensor-map origin one element up.
+//  * Split-K over a deterministic workspace + fixed-order reduction when the
+//    MxN tile count cannot fill 148 SMs.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "utv_internal.h"
+
+namespace utv {
+
+namespace gemm {
+constexpr int BM = 128, BN = 128, BK = 16, STAGES = 5;
+constexpr int NCW = 8;                   // consumer warps
+constexpr int THREADS = NCW * 32;  // thread 0 also issues TMA
+constexpr int A_ST = BM * BK;            // doubles per stage
+constexpr int B_ST = BN * BK;
+constexpr uint32_t STAGE_BYTES = (A_ST + B_ST) * 8;
+constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 + 2 * STAGES * 8 + 64;
+
+struct Args {
+  int M, N, K;
+  int a_sh, b_sh;    // M/N-origin shift of A_N / B_T tiles (0 or 1), see DESIGN.md
+  int k_sh;          // K-origin shift: logical k = k' - k_sh
+  int k_split;       // k' elements per split (multiple of BK)
+  double alpha, beta;
+  double* C;
+  long ldc;
+  double* ws;  // split-K partials [split][N][M] (ld = M)
+};
+
+// Physical double offset inside a 128B-swizzled tile whose 128-byte line is
+// `line` and whose logical element within that line is `idx` (0..15).
+__device__ __forceinline__ int swz(int line, int idx) {
+  return line * 16 + ((((idx >> 1) ^ line) & 7) << 1) + (idx & 1);
+}
+
+// A_N tile [mblk][k][16m]; A_T tile [m][16k]; B_N [n][16k]; B_T [nblk][k][16n].
+template <bool TA>
+__device__ __forceinline__ int a_off_of(int k, int m) {
+  if (TA) return swz(m, k);
+  return swz(((m >> 4) << 4) + k, m & 15);
+}
+template <bool TB>
+__device__ __forceinline__ int b_off_of(int k, int n) {
+  if (!TB) return swz(n, k);
+  return swz(((n >> 4) << 4) + k, n & 15);
+}
+
+// Logical row (0..127) of fragment row r in warp m-tile t.
+template <bool TA>
+__device__ __forceinline__ int frag_row(int wm, int t, int r) {
+  if (TA) return wm * 64 + t * 8 + (r & 3) * 2 + (r >> 2);
+  int mblk = wm * 4 + (t >> 1);
+  return mblk * 16 + (t & 1) * 4 + (r & 1) + ((r >> 1) & 1) * 8 + (r >> 2) * 2;
+}
+template <bool TB>
+__device__ __forceinline__ int frag_col(int wn, int u, int c) {
+  if (!TB) return wn * 32 + u * 8 + (c & 3) * 2 + (c >> 2);
+  int nblk = wn * 2 + (u >> 1);
+  return nblk * 16 + (u & 1) * 4 + (c & 1) + ((c >> 1) & 1) * 8 + (c >> 2) * 2;
+}
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(THREADS, 1)
+    dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA,
+                     const __grid_constant__ CUtensorMap tmB, const Args p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  double* smem = (double*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  double* sA = smem;
+  double* sB = smem + STAGES * A_ST;
+  uint64_t* bars = (uint64_t*)(sB + STAGES * B_ST);
+  const uint32_t full0 = smem_u32(bars);
+  const uint32_t empty0 = smem_u32(bars + STAGES);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // TMA box origins (always 16B aligned) and the logical origin of the tile.
+  const int mc = blockIdx.x * BM, nc = blockIdx.y * BN;
+  const int m0 = mc - (TA ? 0 : p.a_sh), n0 = nc - (TB ? p.b_sh : 0);
+  const int kb = blockIdx.z * p.k_split;
+  const int ke = min(p.K + p.k_sh, kb + p.k_split);
+  const int nk = (ke - kb + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, NCW);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  // Thread 0 doubles as the TMA producer: it keeps STAGES-1 k-blocks in
+  // flight ahead of the consumers (refilling a slot once all 8 warps have
+  // released it through the `empty` mbarrier).
+  auto produce = [&](int it) {
+    const int s = it % STAGES;
+    if (it >= STAGES) mbar_wait(empty0 + 8 * s, ((it / STAGES) & 1) ^ 1);
+    const uint32_t fb = full0 + 8 * s;
+    mbar_arrive_expect_tx(fb, STAGE_BYTES);
+    const int k = kb + it * BK;       // k' (even): K-major operands load at k', others at k'-k_sh
+    const uint32_t dA = smem_u32(sA + s * A_ST), dB = smem_u32(sB + s * B_ST);
+    if (TA) {
+      tma_load_2d(dA, &tmA, fb, k, mc);
+    } else {
+#pragma unroll
+      for (int i = 0; i < BM / 16; ++i) tma_load_2d(dA + i * 2048, &tmA, fb, mc + 16 * i, k - p.k_sh);
+    }
+    if (!TB) {
+      tma_load_2d(dB, &tmB, fb, k, nc);
+    } else {
+#pragma unroll
+      for (int i = 0; i < BN / 16; ++i) tma_load_2d(dB + i * 2048, &tmB, fb, nc + 16 * i, k - p.k_sh);
+    }
+  };
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int it = 0; it < min(nk, STAGES - 1); ++it) produce(it);
+  }
+
+  // ---------------- DMMA consumers ----------------
+  const int wm = warp & 1, wn = warp >> 1;
+  const int fr = lane >> 2, fk = lane & 3;
+  double acc[8][4][2];
+#pragma unroll
+  for (int t = 0; t < 8; ++t)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
+
+  // Per-thread fragment offsets (k-independent parts are folded at use).
+  int arow[8], bcol[4];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) arow[t] = frag_row<TA>(wm, t, fr);
+#pragma unroll
+  for (int u = 0; u < 4; ++u) bcol[u] = frag_col<TB>(wn, u, fr);
+
+  const bool zero_k0 = (p.k_sh != 0) && (blockIdx.z == 0);
+  for (int it = 0; it < nk; ++it) {
+    if (threadIdx.x == 0 && it + STAGES - 1 < nk) produce(it + STAGES - 1);
+    __syncwarp();
+    const int s = it % STAGES;
+    mbar_wait(full0 + 8 * s, (it / STAGES) & 1);
+    const double* a = sA + s * A_ST;
+    const double* b = sB + s * B_ST;
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      const int k = kk * 4 + fk;
+      double af[8], bf[4];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) af[t] = a[a_off_of<TA>(k, arow[t])];
+      // k' = 0 is the logical row k = -1 when the K origin is shifted: when
+      // both operands carry real data there (TN), zero it in registers.
+      if (zero_k0 && it == 0 && kk == 0 && fk == 0) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) af[t] = 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) bf[u] = b[b_off_of<TB>(k, bcol[u])];
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) dmma884(acc[t][u][0], acc[t][u][1], af[t], bf[u]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * s);
+  }
+
+  // ---------------- epilogue ----------------
+  const int crow_l = lane >> 2, ccol_l = (lane & 3) * 2;
+  if (p.ws == nullptr) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int m = m0 + frag_row<TA>(wm, t, crow_l);
+      if (m < 0 || m >= p.M) continue;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int n = n0 + frag_col<TB>(wn, u, ccol_l + j);
+          if (n >= 0 && n < p.N) {
+            double* c = p.C + m + (long)n * p.ldc;
+            const double v = p.alpha * acc[t][u][j];
+            *c = (p.beta == 0.0) ? v : fma(p.beta, *c, v);
+          }
+        }
+      }
+    }
+  } else {
+    double* w = p.ws + (size_t)blockIdx.z * p.N * p.M;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int m = m0 + frag_row<TA>(wm, t, crow_l);
+      if (m < 0 || m >= p.M) continue;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int n = n0 + frag_col<TB>(wn, u, ccol_l + j);
+          if (n >= 0 && n < p.N) w[m + (size_t)n * p.M] = acc[t][u][j];
+        }
+    }
+  }
+}
+
+// C = alpha * sum_s ws[s] + beta * C, summed in split order (deterministic).
+__global__ void splitk_reduce_kernel(const double* __restrict__ ws, int splits, int M, int N,
+                                     double alpha, double beta, double* C, long ldc) {
+  const size_t total = (size_t)M * N;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int z = 0; z < splits; ++z) s += ws[(size_t)z * total + i];
+    const int m = (int)(i % M), n = (int)(i / M);
+    double* c = C + m + (long)n * ldc;
+    const double v = alpha * s;
+    *c = (beta == 0.0) ? v : fma(beta, *c, v);
+  }
+}
+
+__global__ void scale_kernel(int M, int N, double beta, double* C, long ldc) {
+  const size_t total = (size_t)M * N;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int m = (int)(i % M), n = (int)(i / M);
+    double* c = C + m + (long)n * ldc;
+    *c = (beta == 0.0) ? 0.0 : beta * *c;
+  }
+}
+
+}  // namespace gemm
+
+// ---------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static std::once_flag g_encode_once;
+static int g_num_sms = 0;
+
+static int get_encode() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    for (auto f : {gemm::dgemm_tma_kernel<false, false>, gemm::dgemm_tma_kernel<false, true>,
+                   gemm::dgemm_tma_kernel<true, false>, gemm::dgemm_tma_kernel<true, true>})
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm::SMEM_BYTES);
+  });
+  return g_encode ? UTV_OK : UTV_ERR_CUDA;
+}
+
+int num_sms() {
+  get_encode();
+  return g_num_sms > 0 ? g_num_sms : 148;
+}
+
+// Tensor map over a column-major (rows x cols) matrix with leading dim ld.
+// TMA needs a 16B-aligned origin and 16B-aligned box starts in dim0, so an
+// 8B-aligned (odd-row) sub-matrix is mapped from one element above; *shift
+// returns that offset (0/1).  Box starts stay even; the kernel shifts its
+// logical tile origin instead (M/N dims) or runs the K loop over k' = k +
+// shift with the other operand reading k' - shift (TMA zero-fills the
+// out-of-range k = -1 slot, so the extra row contributes exactly 0).
+static int make_map(CUtensorMap* map, const double* p, long rows, long cols, long ld,
+                    uint32_t box0, uint32_t box1, int* shift) {
+  if ((ld & 1) || ((uintptr_t)p & 7)) return UTV_ERR_ALIGN;
+  int sh = ((uintptr_t)p & 15) ? 1 : 0;
+  const double* base = p - sh;
+  cuuint64_t dims[2] = {(cuuint64_t)(rows + sh), (cuuint64_t)cols};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 8)};
+  cuuint32_t box[2] = {box0, box1};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)base, dims, strides, box,
+                        es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    fprintf(stderr, "libutvb200: cuTensorMapEncodeTiled failed (%d) rows=%ld cols=%ld ld=%ld\n",
+            (int)r, rows, cols, ld);
+    return UTV_ERR_CUDA;
+  }
+  *shift = sh;
+  return UTV_OK;
+}
+
+size_t dgemm_ws_doubles(int M, int N, int K) {
+  // Upper bound of split-K workspace chosen by dgemm() below.
+  int tiles = ceil_div(M, gemm::BM) * ceil_div(N, gemm::BN);
+  int splits = choose_splits(tiles, K);
+  return splits > 1 ? (size_t)splits * M * N : 0;
+}
+
+int choose_splits(int tiles, int K) {
+  const int sms = num_sms();
+  const int kblocks = ceil_div(K, gemm::BK);
+  if (tiles >= sms || kblocks < 8) return 1;
+  // Pick the split count (each split keeps >= 8 k-blocks) maximising wave
+  // efficiency; ties go to fewer splits.
+  int best = 1;
+  double best_eff = (double)tiles / (ceil_div(tiles, sms) * sms);
+  for (int s = 2; s <= 64 && kblocks / s >= 8; ++s) {
+    const int units = tiles * s;
+    const double eff = (double)units / (ceil_div(units, sms) * sms);
+    // prefer more work per CTA when efficiency is equal
+    if (eff > best_eff + 0.02) {
+      best = s;
+      best_eff = eff;
+    }
+    if (units >= 2 * sms && eff > 0.9) break;
+  }
+  return best;
+}
+
+int dgemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, long lda,
+          const double* B, long ldb, double beta, double* C, long ldc, double* ws,
+          size_t ws_doubles, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return UTV_OK;
+  UTV_CHECK(get_encode());
+  if (K <= 0 || alpha == 0.0) {
+    if (beta == 1.0) return UTV_OK;
+    gemm::scale_kernel<<<min(4 * num_sms(), ceil_div((long)M * N, 256)), 256, 0, st>>>(M, N, beta, C, ldc);
+    UTV_CUDA(cudaGetLastError());
+    return UTV_OK;
+  }
+  // TN with K-origins of different parity: re-stage the smaller operand with
+  // the other's parity (rare: only odd block sizes / odd user offsets).
+  const double* Ause = A;
+  long ldause = lda;
+  const double* Buse = B;
+  long ldbuse = ldb;
+  double* tmp = nullptr;
+  if (ta && !tb && (((uintptr_t)A & 15) != 0) != (((uintptr_t)B & 15) != 0)) {
+    const bool copyA = (long)K * M <= (long)K * N;
+    const int sh = copyA ? (((uintptr_t)B & 15) ? 1 : 0) : (((uintptr_t)A & 15) ? 1 : 0);
+    const long cols = copyA ? M : N;
+    const long ldt = round_up(K + 1, 2);
+    UTV_CUDA(cudaMallocAsync((void**)&tmp, sizeof(double) * (ldt * cols + 2), st));
+    double* dst = tmp + sh;
+    UTV_CHECK(copy_mat(copyA ? A : B, copyA ? lda : ldb, dst, ldt, K, (int)cols, st));
+    if (copyA) { Ause = dst; ldause = ldt; } else { Buse = dst; ldbuse = ldt; }
+  }
+  CUtensorMap mA, mB;
+  int shA = 0, shB = 0;
+  if (ta) UTV_CHECK(make_map(&mA, Ause, K, M, ldause, 16, gemm::BM, &shA));
+  else UTV_CHECK(make_map(&mA, Ause, M, K, ldause, 16, 16, &shA));
+  if (tb) UTV_CHECK(make_map(&mB, Buse, N, K, ldbuse, 16, 16, &shB));
+  else UTV_CHECK(make_map(&mB, Buse, K, N, ldbuse, 16, gemm::BN, &shB));
+  const int a_sh = ta ? 0 : shA, b_sh = tb ? shB : 0;
+  const int k_sh = ta ? shA : (!tb ? shB : 0);
+
+  const int tm = ceil_div(M + a_sh, gemm::BM), tn = ceil_div(N + b_sh, gemm::BN);
+  const int Kp = K + k_sh;
+  int splits = choose_splits(tm * tn, Kp);
+  if (ws == nullptr) splits = 1;
+  while (splits > 1 && (size_t)splits * M * N > ws_doubles) --splits;
+  int kper = (int)round_up(ceil_div(Kp, splits), gemm::BK);
+  splits = ceil_div(Kp, kper);
+
+  gemm::Args a;
+  a.M = M; a.N = N; a.K = K;
+  a.a_sh = a_sh; a.b_sh = b_sh; a.k_sh = k_sh;
+  a.k_split = kper;
+  a.alpha = alpha; a.beta = beta;
+  a.C = C; a.ldc = ldc;
+  a.ws = splits > 1 ? ws : nullptr;
+  dim3 grid(tm, tn, splits);
+  if (!ta && !tb) gemm::dgemm_tma_kernel<false, false><<<grid, gemm::THREADS, gemm::SMEM_BYTES, st>>>(mA, mB, a);
+  else if (!ta && tb) gemm::dgemm_tma_kernel<false, true><<<grid, gemm::THREADS, gemm::SMEM_BYTES, st>>>(mA, mB, a);
+  else if (ta && !tb) gemm::dgemm_tma_kernel<true, false><<<grid, gemm::THREADS, gemm::SMEM_BYTES, st>>>(mA, mB, a);
+  else gemm::dgemm_tma_kernel<true, true><<<grid, gemm::THREADS, gemm::SMEM_BYTES, st>>>(mA, mB, a);
+  UTV_CUDA(cudaGetLastError());
+  if (splits > 1) {
+    const long total = (long)M * N;
+    gemm::splitk_reduce_kernel<<<min(8 * num_sms(), ceil_div(total, 256)), 256, 0, st>>>(
+        ws, splits, M, N, alpha, beta, C, ldc);
+    UTV_CUDA(cudaGetLastError());
+  }
+  if (tmp) UTV_CUDA(cudaFreeAsync(tmp, st));
+  return UTV_OK;
+}
+
+}  // namespace utv

@@ -1,0 +1,145 @@
+// K7: small fused ops on column-major blocks (HBM-bound, vectorised grid-stride).
+//  * sumsq: deterministic Frobenius reductions (ErrorTracker, randutv.py:52-62;
+//    qr.py:86 threshold; record_trailing randutv.py:160-161).
+//  * structured writes: identity (randutv.py:115-116), zero blocks
+//    (randutv.py:149), diag(sigma) (randutv.py:154,169-171), block copies.
+#include "common.cuh"
+#include "utv_internal.h"
+
+namespace utv {
+
+namespace ops {
+constexpr int RED_BLOCKS = 296;  // 2 x 148 SMs; fixed so the reduction order is fixed
+constexpr int RED_THREADS = 512;
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = (l < (int)(blockDim.x >> 5)) ? sh[l] : 0.0;
+    v = warp_sum(v);
+  }
+  __syncthreads();
+  return v;
+}
+
+// Partial sums of squares: block b handles columns b, b+G, ... (one warp row
+// sweep per column, coalesced along the contiguous dimension).
+__global__ void sumsq_partial(const double* __restrict__ A, long lda, int rows, int cols,
+                              double* __restrict__ part) {
+  __shared__ double sh[32];
+  double acc = 0.0;
+  const long total = (long)rows * cols;
+  if (rows >= 256) {
+    for (int c = blockIdx.x; c < cols; c += gridDim.x) {
+      const double* col = A + (long)c * lda;
+      for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+        const double x = col[r];
+        acc = fma(x, x, acc);
+      }
+    }
+  } else {
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total;
+         i += (long)gridDim.x * blockDim.x) {
+      const double x = A[(i % rows) + (i / rows) * lda];
+      acc = fma(x, x, acc);
+    }
+  }
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+__global__ void sum_partials(const double* __restrict__ part, int n, double* out) {
+  __shared__ double sh[32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += part[i];
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) *out = acc;
+}
+
+__global__ void fill_kernel(double* A, long lda, int rows, int cols, double diag_val,
+                            double off_val) {
+  const long total = (long)rows * cols;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total;
+       i += (long)gridDim.x * blockDim.x) {
+    const int r = (int)(i % rows), c = (int)(i / rows);
+    A[r + (long)c * lda] = (r == c) ? diag_val : off_val;
+  }
+}
+
+__global__ void diag_kernel(double* A, long lda, int rows, int cols, const double* d) {
+  const long total = (long)rows * cols;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total;
+       i += (long)gridDim.x * blockDim.x) {
+    const int r = (int)(i % rows), c = (int)(i / rows);
+    A[r + (long)c * lda] = (r == c) ? d[r] : 0.0;
+  }
+}
+
+__global__ void copy_kernel(const double* __restrict__ S, long lds, double* __restrict__ D,
+                            long ldd, int rows, int cols) {
+  const long total = (long)rows * cols;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total;
+       i += (long)gridDim.x * blockDim.x) {
+    const int r = (int)(i % rows), c = (int)(i / rows);
+    D[r + (long)c * ldd] = S[r + (long)c * lds];
+  }
+}
+
+inline int grid_for(long total) {
+  const long g = (total + 255) / 256;
+  const long cap = 8L * num_sms();
+  return (int)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+}  // namespace ops
+
+size_t sumsq_scratch_doubles() { return ops::RED_BLOCKS; }
+
+int sumsq(const double* A, long lda, int rows, int cols, double* out, double* scratch,
+          cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) {
+    UTV_CUDA(cudaMemsetAsync(out, 0, sizeof(double), st));
+    return UTV_OK;
+  }
+  ops::sumsq_partial<<<ops::RED_BLOCKS, ops::RED_THREADS, 0, st>>>(A, lda, rows, cols, scratch);
+  UTV_CUDA(cudaGetLastError());
+  ops::sum_partials<<<1, 512, 0, st>>>(scratch, ops::RED_BLOCKS, out);
+  UTV_CUDA(cudaGetLastError());
+  return UTV_OK;
+}
+
+int set_identity(double* A, long lda, int rows, int cols, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return UTV_OK;
+  ops::fill_kernel<<<ops::grid_for((long)rows * cols), 256, 0, st>>>(A, lda, rows, cols, 1.0, 0.0);
+  UTV_CUDA(cudaGetLastError());
+  return UTV_OK;
+}
+
+int set_zero(double* A, long lda, int rows, int cols, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return UTV_OK;
+  if (lda == rows) {
+    UTV_CUDA(cudaMemsetAsync(A, 0, sizeof(double) * rows * (size_t)cols, st));
+    return UTV_OK;
+  }
+  UTV_CUDA(cudaMemset2DAsync(A, lda * sizeof(double), 0, rows * sizeof(double), cols, st));
+  return UTV_OK;
+}
+
+int copy_mat(const double* src, long lds, double* dst, long ldd, int rows, int cols,
+             cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return UTV_OK;
+  UTV_CUDA(cudaMemcpy2DAsync(dst, ldd * sizeof(double), src, lds * sizeof(double),
+                             rows * sizeof(double), cols, cudaMemcpyDeviceToDevice, st));
+  return UTV_OK;
+}
+
+int set_diag(double* A, long lda, int nr, int nc, const double* d, cudaStream_t st) {
+  if (nr <= 0 || nc <= 0) return UTV_OK;
+  ops::diag_kernel<<<ops::grid_for((long)nr * nc), 256, 0, st>>>(A, lda, nr, nc, d);
+  UTV_CUDA(cudaGetLastError());
+  return UTV_OK;
+}
+
+}  // namespace utv

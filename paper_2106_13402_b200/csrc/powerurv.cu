@@ -1,0 +1,92 @@
+// Device driver for powerURV (Algorithm 1 of arXiv 2106.13402; reference
+// powerurv.py:41-72), one stream, no host synchronisation.
+//
+//   q == 0: Vq = hqr_full(G)
+//   else  : V = G; q x { Yhat = A V; Vhat = thinQ(Yhat); Y = A^T Vhat;
+//                        Vq = hqr_full(Y); V = Q(Vq) (skipped after the last
+//                        round: the reference's last materialisation is dead,
+//                        powerurv.py:68-70) }
+//   Ahat = A Q(Vq) via compact WY (powerurv.py:70); (Uq, R) = hqr_full(Ahat).
+#include "common.cuh"
+#include "utv_internal.h"
+
+namespace utv {
+
+struct PurvWs {
+  double *Yh, *Yq, *Tq, *Vh, *Vc, *Yn, *gws, *qr, *lfb, *org;
+  long ldm, ldn;
+  size_t qr_n, lfb_n, org_n;
+};
+
+static size_t plan_purv(int m, int n, PurvWs* w, double* base) {
+  size_t used = 0;
+  auto take = [&](size_t nd) -> double* {
+    double* p = base ? (double*)((char*)base + used) : nullptr;
+    used += round_up((long)(nd * sizeof(double)), 256);
+    return p;
+  };
+  PurvWs v;
+  v.ldm = round_up(m, 4);
+  v.ldn = round_up(n, 4);
+  v.qr_n = geqrf_ws_doubles(m, n, true);
+  v.lfb_n = larfb_ws_doubles(m, n, n);
+  v.org_n = (size_t)v.ldn * n + SPLITK_WS + 1024;
+  v.Yh = take(v.ldm * n);
+  v.Yq = take(v.ldm * n);
+  v.Tq = take(v.ldn * n);
+  v.Vh = take(v.ldm * n);
+  v.Vc = take(v.ldn * n);
+  v.Yn = take(v.ldn * n);
+  v.gws = take(SPLITK_WS);
+  v.qr = take(v.qr_n);
+  v.lfb = take(v.lfb_n);
+  v.org = take(v.org_n);
+  if (w) *w = v;
+  return used / sizeof(double) + 64;
+}
+
+size_t powerurv_ws_doubles(int m, int n) { return plan_purv(m, n, nullptr, nullptr); }
+
+int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, Mat Vt, double* ws,
+             size_t ws_doubles, cudaStream_t st) {
+  if (m < n) return -1;
+  if (q < 0) return -3;
+  if (ws_doubles < plan_purv(m, n, nullptr, nullptr)) return UTV_ERR_WORKSPACE;
+  PurvWs w;
+  plan_purv(m, n, &w, ws);
+  if (q == 0) {
+    // Vq = hqr_full(G) (powerurv.py:58-59); G is read-only -> work on a copy
+    UTV_CHECK(copy_mat(G.p, G.ld, w.Yn, w.ldn, n, n, st));
+    UTV_CHECK(geqrf(Mat{w.Yn, w.ldn, n, n}, Vy, Vt, true, w.qr, w.qr_n, st));
+  } else {
+    const double* vcur = G.p;
+    long ldv = G.ld;
+    for (int it = 0; it < q; ++it) {
+      // Yhat = A V (powerurv.py:64)
+      UTV_CHECK(dgemm(false, false, m, n, n, 1.0, A.p, A.ld, vcur, ldv, 0.0, w.Yh, w.ldm, w.gws,
+                      SPLITK_WS, st));
+      // Vhat = thin Q of Yhat (powerurv.py:65)
+      Mat Yq{w.Yq, w.ldm, m, n}, Tq{w.Tq, w.ldn, n, n};
+      UTV_CHECK(geqrf(Mat{w.Yh, w.ldm, m, n}, Yq, Tq, true, w.qr, w.qr_n, st));
+      UTV_CHECK(orgqr(Yq, Tq, Mat{w.Vh, w.ldm, m, n}, w.org, w.org_n, st));
+      // Y = A^T Vhat (powerurv.py:66)
+      UTV_CHECK(dgemm(true, false, n, n, m, 1.0, A.p, A.ld, w.Vh, w.ldm, 0.0, w.Yn, w.ldn, w.gws,
+                      SPLITK_WS, st));
+      // Vq = hqr_full(Y) (powerurv.py:67)
+      UTV_CHECK(geqrf(Mat{w.Yn, w.ldn, n, n}, Vy, Vt, true, w.qr, w.qr_n, st));
+      if (it + 1 < q) {
+        UTV_CHECK(orgqr(Vy, Vt, Mat{w.Vc, w.ldn, n, n}, w.org, w.org_n, st));
+        vcur = w.Vc;
+        ldv = w.ldn;
+      }
+    }
+  }
+  // Ahat = A Q(Vq) (powerurv.py:70), formed in R's storage
+  UTV_CHECK(copy_mat(A.p, A.ld, R.p, R.ld, m, n, st));
+  UTV_CHECK(larfb('R', false, Vy, Vt, R, w.lfb, w.lfb_n, st));
+  // (Uq, R) = hqr_full(Ahat) (powerurv.py:71)
+  UTV_CHECK(geqrf(R, Uy, Ut, true, w.qr, w.qr_n, st));
+  return UTV_OK;
+}
+
+}  // namespace utv

@@ -1,0 +1,59 @@
+// Internal (C++) interfaces shared by the libutvb200 translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+
+#include "common.cuh"
+
+namespace utv {
+
+int num_sms();
+
+// Split-K scratch reserved by every multi-GEMM routine (300 tiles of 128x128).
+constexpr size_t SPLITK_WS = 300ull * 128 * 128;
+
+// ---- K1 GEMM (gemm.cu) ----
+int choose_splits(int tiles, int K);
+size_t dgemm_ws_doubles(int M, int N, int K);
+int dgemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, long lda,
+          const double* B, long ldb, double beta, double* C, long ldc, double* ws,
+          size_t ws_doubles, cudaStream_t st);
+
+// ---- small device ops (ops.cu) ----
+// out[0] = sum of squares of the rows x cols block (deterministic two-pass).
+int sumsq(const double* A, long lda, int rows, int cols, double* out, double* scratch,
+          cudaStream_t st);
+size_t sumsq_scratch_doubles();
+int set_identity(double* A, long lda, int rows, int cols, cudaStream_t st);
+int set_zero(double* A, long lda, int rows, int cols, cudaStream_t st);
+int copy_mat(const double* src, long lds, double* dst, long ldd, int rows, int cols,
+             cudaStream_t st);
+// diag block: A[:nr, :nc] = 0 except A[i,i] = d[i] (i < min(nr, nc)).
+int set_diag(double* A, long lda, int nr, int nc, const double* d, cudaStream_t st);
+
+// ---- K3 panel QR + K4 blocked QR (qr.cu) ----
+// Householder QR of the rows x cols panel P (rows >= cols), in place:
+// P <- R (zeros below the diagonal); Y (rows x cols, unit lower, zeros above)
+// and the forward compact-WY triangle Tw (cols x cols) are written out.
+// thr_src: device scalar holding ||input||_F^2 (threshold = eps*sqrt(.)).
+size_t geqrf_ws_doubles(int rows, int cols, bool want_t);
+int geqrf(Mat P, Mat Y, Mat Tw, bool want_t, double* ws, size_t ws_doubles, cudaStream_t st);
+
+// ---- K2 compact-WY apply (qr.cu) ----
+// side 'L': B <- Q^(T) B ; side 'R': B <- B Q^(T);  Q = I - Y T Y^T, Y is k x w.
+size_t larfb_ws_doubles(int brows, int bcols, int w);
+int larfb(char side, bool trans, Mat Y, Mat T, Mat B, double* ws, size_t ws_doubles,
+          cudaStream_t st);
+// Q[:, :ncols] = I - Y (T Y[:ncols,:]^T)
+int orgqr(Mat Y, Mat T, Mat Q, double* ws, size_t ws_doubles, cudaStream_t st);
+
+// ---- K6 Jacobi SVD (jacobi.cu) ----
+// A (n x n, read only): sigma (desc, device), U (n x n), V (n x n) with the
+// reference sign rule (svd.py:53-57).  *status_dev (device int) receives the
+// number of sweeps used, or -1 if the sweep cap was hit (no host sync here).
+size_t gesvj_ws_doubles(int n);
+int gesvj(Mat A, double* sigma, Mat U, Mat V, double* ws, size_t ws_doubles, int* status_dev,
+          cudaStream_t st);
+
+}  // namespace utv

@@ -1,0 +1,151 @@
+"""Device-resident operations over ``DMat`` (column-major FP64 in HBM).
+
+Each function is a thin wrapper over one C-ABI entry point of libutvb200
+(include/utv_b200.h).  The numpy-facing drop-in API (qr.py, svd.py,
+powerurv.py, randutv.py) and bench.py are built on these.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from ._lib import DMat, check, dempty, load, stream_ptr, workspace
+
+
+def gemm(transa, transb, alpha, A: DMat, B: DMat, beta=0.0, C: DMat | None = None,
+         m=None, n=None, k=None):
+    lib = load()
+    ta, tb = transa.upper() == "T", transb.upper() == "T"
+    m = (A.cols if ta else A.rows) if m is None else m
+    k = (A.rows if ta else A.cols) if k is None else k
+    n = (B.rows if tb else B.cols) if n is None else n
+    if C is None:
+        C = dempty(m, n)
+        beta = 0.0
+    lw = lib.utv_dgemm_bufsize(m, n, k)
+    ws = workspace(lw)
+    check(lib.utv_dgemm(transa.encode(), transb.encode(), m, n, k, alpha, A.ptr, A.ld, B.ptr, B.ld,
+                        beta, C.ptr, C.ld, ws.data_ptr(), lw, stream_ptr()), "utv_dgemm")
+    return C
+
+
+def sumsq(A: DMat):
+    import torch
+    lib = load()
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    lw = lib.utv_dsumsq_bufsize()
+    ws = workspace(lw)
+    check(lib.utv_dsumsq(A.rows, A.cols, A.ptr, A.ld, out.data_ptr(), ws.data_ptr(), lw,
+                         stream_ptr()), "utv_dsumsq")
+    return out
+
+
+def geqrf(A: DMat):
+    """In place: A <- R. Returns (Y, T)."""
+    lib = load()
+    m, n = A.rows, A.cols
+    Y = dempty(m, n)
+    T = dempty(n, n)
+    lw = lib.utv_dgeqrf_bufsize(m, n)
+    ws = workspace(lw)
+    check(lib.utv_dgeqrf(m, n, A.ptr, A.ld, Y.ptr, Y.ld, T.ptr, T.ld, ws.data_ptr(), lw,
+                         stream_ptr()), "utv_dgeqrf")
+    return Y, T
+
+
+def larfb(side, trans, Y: DMat, T: DMat, B: DMat):
+    lib = load()
+    lw = lib.utv_dlarfb_bufsize(B.rows, B.cols, Y.cols)
+    ws = workspace(lw)
+    check(lib.utv_dlarfb(side.encode(), b"T" if trans else b"N", B.rows, B.cols, Y.rows, Y.cols,
+                         Y.ptr, Y.ld, T.ptr, T.ld, B.ptr, B.ld, ws.data_ptr(), lw, stream_ptr()),
+          "utv_dlarfb")
+    return B
+
+
+def orgqr(Y: DMat, T: DMat, ncols):
+    lib = load()
+    Q = dempty(Y.rows, ncols)
+    lw = lib.utv_dorgqr_bufsize(Y.rows, ncols, Y.cols)
+    ws = workspace(lw)
+    check(lib.utv_dorgqr(Y.rows, ncols, Y.cols, Y.ptr, Y.ld, T.ptr, T.ld, Q.ptr, Q.ld,
+                         ws.data_ptr(), lw, stream_ptr()), "utv_dorgqr")
+    return Q
+
+
+def gesvj(A: DMat):
+    """Returns (sigma tensor, U, V, status tensor)."""
+    import torch
+    lib = load()
+    n = A.rows
+    sig = torch.empty(max(n, 1), dtype=torch.float64, device="cuda")
+    U = dempty(n, n)
+    V = dempty(n, n)
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    lw = lib.utv_dgesvj_bufsize(n)
+    ws = workspace(lw)
+    check(lib.utv_dgesvj(n, A.ptr, A.ld, sig.data_ptr(), U.ptr, U.ld, V.ptr, V.ld,
+                         status.data_ptr(), ws.data_ptr(), lw, stream_ptr()), "utv_dgesvj")
+    return sig, U, V, status
+
+
+def stage_randutv_blocks(blocks, b):
+    """Concatenate the C-order k_i x b Gaussian draws into one b x sum(k_i)
+    column-major device matrix (block i = G_i^T); ld padded to even."""
+    torch_ = _lib.torch_cuda()
+    total = sum(int(g.shape[0]) for g in blocks)
+    G = dempty(b, max(total, 1))
+    col = 0
+    for g in blocks:
+        g = np.ascontiguousarray(g, dtype=np.float64)       # C order: rows of length b
+        k = g.shape[0]
+        G.t[col:col + k, :b].copy_(torch_.from_numpy(g))
+        col += k
+    return G
+
+
+class RandUtvRun:
+    """Device buffers + workspace for repeated randUTV runs of one shape."""
+
+    def __init__(self, m, n, b, q, record_trailing=False):
+        import torch
+        self.m, self.n, self.b, self.q = m, n, b, q
+        lib = load()
+        self.lw = lib.utv_randutv_basic_bufsize(m, n, b, q)
+        self.ws = workspace(self.lw)
+        steps = -(-n // b)
+        self.steps = steps
+        self.errsq = torch.zeros(steps, dtype=torch.float64, device="cuda")
+        self.trail2 = torch.zeros(steps, dtype=torch.float64, device="cuda") if record_trailing else None
+        self.status = torch.zeros(steps, dtype=torch.int32, device="cuda")
+
+    def run(self, T: DMat, U: DMat, V: DMat, G: DMat):
+        lib = load()
+        check(lib.utv_randutv_basic_f64(
+            self.m, self.n, self.b, self.q, T.ptr, T.ld, U.ptr, U.ld, V.ptr, V.ld, G.ptr, G.ld,
+            self.errsq.data_ptr(), self.trail2.data_ptr() if self.trail2 is not None else None,
+            self.status.data_ptr(), self.ws.data_ptr(), self.lw, stream_ptr()),
+            "utv_randutv_basic_f64")
+
+
+class PowerUrvRun:
+    """Device workspace for repeated powerURV runs of one shape."""
+
+    def __init__(self, m, n, q):
+        lib = load()
+        self.m, self.n, self.q = m, n, q
+        self.lw = lib.utv_powerurv_bufsize(m, n, q)
+        self.ws = workspace(self.lw)
+        self.Uy = dempty(m, n)
+        self.Ut = dempty(n, n)
+        self.R = dempty(m, n)
+        self.Vy = dempty(n, n)
+        self.Vt = dempty(n, n)
+
+    def run(self, A: DMat, G: DMat):
+        lib = load()
+        check(lib.utv_powerurv_f64(
+            self.m, self.n, self.q, A.ptr, A.ld, G.ptr, G.ld, self.Uy.ptr, self.Uy.ld, self.Ut.ptr,
+            self.Ut.ld, self.R.ptr, self.R.ld, self.Vy.ptr, self.Vy.ld, self.Vt.ptr, self.Vt.ld,
+            self.ws.data_ptr(), self.lw, stream_ptr()), "utv_powerurv_f64")

@@ -1,0 +1,114 @@
+"""Generate golden vectors by running the REFERENCE package (utvkit) itself.
+
+Run in the build container, where /root/reference exists:
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+Writes small .npz fixtures next to this script.  The GPU box never reads
+/root/reference; it only reads these committed fixtures.  Each fixture
+records the reference call that produced it (``call`` key).
+"""
+
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def main():
+    sys.dont_write_bytecode = True
+    sys.path.insert(0, REF)
+    import utvkit as uk  # noqa: E402  (reference, read-only)
+
+    def save(name, **kw):
+        path = os.path.join(OUT, name + ".npz")
+        np.savez_compressed(path, **kw)
+        print("wrote", path, os.path.getsize(path), "bytes")
+
+    # ---- hqr_full (qr.py:71-100) -----------------------------------------
+    cases = {}
+    rng = np.random.default_rng(11)
+    cases["eye4"] = np.eye(4)
+    cases["col34"] = np.array([[3.0], [4.0]])
+    cases["rand100x60"] = rng.standard_normal((100, 60))
+    rd = rng.standard_normal((40, 24))
+    rd[:, 5] = 0.0                      # exactly zero column -> skip rule
+    rd[:, 9] = rd[:, 2] * 2.0           # dependent column
+    rd[:, 17:] = 0.0                    # trailing zero block
+    cases["rankdef40x24"] = rd
+    e1 = np.zeros((6, 3)); e1[0, 0] = 2.0; e1[1, 1] = -1.0; e1[:, 2] = 1.0
+    cases["collinear6x3"] = e1          # sigma == 0 columns -> skip rule
+    neg = rng.standard_normal((33, 33))
+    neg[0, 0] = -abs(neg[0, 0]) * 10
+    cases["square33"] = neg
+    for key, a in cases.items():
+        q, r = uk.hqr_full(a)
+        save("hqr_" + key, A=a, Y=q.Y, Twy=q.Twy, R=r, call="hqr_full(A)")
+
+    # ---- apply_q / materialize_q (qr.py:103-131) ------------------------
+    a = rng.standard_normal((50, 30))
+    q, _ = uk.hqr_full(a)
+    bl = rng.standard_normal((50, 7))
+    br = rng.standard_normal((9, 50))
+    save("applyq_50x30", A=a, BL=bl, BR=br,
+         left=uk.apply_q(q, bl, "left", False),
+         left_t=uk.apply_q(q, bl, "left", True),
+         right=uk.apply_q(q, br, "right", False),
+         right_t=uk.apply_q(q, br, "right", True),
+         Q=uk.materialize_q(q), Q30=uk.materialize_q(q, 30),
+         call="apply_q / materialize_q on hqr_full(A)")
+
+    # ---- svd_dense (svd.py:37-58) -------------------------------------
+    svd_cases = {
+        "diag321": np.diag([3.0, 2.0, 1.0]),
+        "rand20": rng.standard_normal((20, 20)),
+        "rank1": np.outer(rng.standard_normal(12), rng.standard_normal(12)),
+        "zero5": np.zeros((5, 5)),
+        "upper64": np.triu(rng.standard_normal((64, 64))),
+        "tall30x8": rng.standard_normal((30, 8)),
+    }
+    for key, a in svd_cases.items():
+        s = uk.svd_dense(a, mode="full")
+        save("svd_" + key, A=a, U=s.U, sigma=s.sigma, V=s.V, call="svd_dense(A,'full')")
+
+    # ---- power_urv_from_sample (powerurv.py:41-72) ----------------------
+    purv = [("gauss120x80_q1", 120, 80, 1, 21), ("gauss96_q2", 96, 96, 2, 22),
+            ("gauss64x48_q0", 64, 48, 0, 23), ("tall200x40_q2", 200, 40, 2, 24)]
+    for key, m, n, qq, seed in purv:
+        st = uk.RngStream(seed)
+        a = uk.gaussian(m, n, st)
+        g = uk.gaussian(n, n, st)
+        f = uk.power_urv_from_sample(a, qq, g)
+        save("purv_" + key, A=a, G=g, q=qq, Uy=f.Uq.Y, Ut=f.Uq.Twy, R=f.R,
+             Vy=f.Vq.Y, Vt=f.Vq.Twy, call=f"power_urv_from_sample(A,{qq},G)")
+    # power_urv with an RngStream: G is gaussian(n, n, rng) (powerurv.py:75-79)
+    a, _ = uk.gen_fast_decay(80, 1e-5, uk.RngStream(5))
+    f = uk.power_urv(a, 2, uk.RngStream(6))
+    save("purv_fast80_q2_seed6", A=a, seed=6, q=2, Uy=f.Uq.Y, Ut=f.Uq.Twy,
+         R=f.R, Vy=f.Vq.Y, Vt=f.Vq.Twy, call="power_urv(A,2,RngStream(6))")
+
+    # ---- randutv_basic (randutv.py:110-193, 228-235) --------------------
+    rutv = []
+    st = uk.RngStream(31)
+    rutv.append(("gauss150x100_b30_q1", uk.gaussian(150, 100, st), 30, 1, 32))
+    rutv.append(("gauss300_b64_q1", uk.gaussian(300, 300, uk.RngStream(33)), 64, 1, 34))
+    rutv.append(("tall300x260_b64_q2", uk.gaussian(300, 260, uk.RngStream(35)), 64, 2, 36))
+    fd, _ = uk.gen_fast_decay(200, 1e-5, uk.RngStream(37))
+    rutv.append(("fast200_b50_q2", fd, 50, 2, 38))
+    rutv.append(("single64_b64_q1", uk.gaussian(64, 64, uk.RngStream(39)), 64, 1, 40))
+    rutv.append(("gauss97_b16_q0", uk.gaussian(97, 97, uk.RngStream(41)), 16, 0, 42))
+    rk = uk.gaussian(120, 30, uk.RngStream(43)) @ uk.gaussian(30, 120, uk.RngStream(44))
+    rutv.append(("rank30_120_b32_q1", rk, 32, 1, 45))
+    for key, a, b, qq, seed in rutv:
+        f = uk.randutv_basic(a, b, qq, uk.RngStream(seed), record_trailing=True)
+        save("rutv_" + key, A=a, b=b, q=qq, seed=seed, U=f.U, T=f.T, V=f.V,
+             errors=np.array(f.errors), trailing=np.array(f.trailing_fro),
+             steps=f.steps_done, efro=uk.bench.trailing_fro_curve(f.T),
+             call=f"randutv_basic(A,{b},{qq},RngStream({seed}),record_trailing=True)")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,194 @@
+"""GPU parity of the individual kernels through the C ABI (K1 GEMM, K3/K4
+geqrf, K2 larfb, K5 orgqr, K6 Jacobi SVD) against the reference's golden
+vectors and numpy fp64."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dv():
+    import paper_2106_13402_b200.device as dv
+    return dv
+
+
+def _dm(a):
+    from paper_2106_13402_b200._lib import dfrom_numpy
+    return dfrom_numpy(a)
+
+
+GEMM_SHAPES = [
+    (1, 1, 1), (7, 5, 3), (128, 128, 16), (129, 130, 17), (300, 64, 1000),
+    (64, 256, 4096), (256, 256, 8192), (1000, 300, 77), (513, 257, 255), (33, 700, 2048),
+]
+
+
+@pytest.mark.parametrize("ta", [False, True])
+@pytest.mark.parametrize("tb", [False, True])
+@pytest.mark.parametrize("shape", GEMM_SHAPES)
+def test_dgemm_matches_numpy(dv, ta, tb, shape):
+    m, n, k = shape
+    rng = np.random.default_rng(m * 7 + n * 3 + k)
+    A = rng.standard_normal((k, m) if ta else (m, k))
+    B = rng.standard_normal((n, k) if tb else (k, n))
+    C0 = rng.standard_normal((m, n))
+    ref = 1.5 * ((A.T if ta else A) @ (B.T if tb else B)) - 0.5 * C0
+    C = _dm(C0)
+    dv.gemm("T" if ta else "N", "T" if tb else "N", 1.5, _dm(A), _dm(B), beta=-0.5, C=C)
+    out = C.to_numpy()
+    # forward error bound of a dot product of length k
+    bound = 4 * k * np.finfo(float).eps * (np.abs(A).max() * np.abs(B).max() * 1.5 + 1)
+    assert np.abs(out - ref).max() <= bound * max(1.0, np.sqrt(k))
+
+
+def test_dgemm_unaligned_submatrices(dv):
+    """Odd row offsets (pointer not 16B aligned) and ragged edges."""
+    from paper_2106_13402_b200._lib import DMat, check, load, stream_ptr, workspace
+    rng = np.random.default_rng(5)
+    big = rng.standard_normal((301, 260))
+    Bm = rng.standard_normal((260, 90))
+    dA, dB = _dm(big), _dm(Bm)
+    for (r0, c0, m, k) in [(1, 3, 200, 150), (3, 0, 77, 257), (0, 1, 300, 33)]:
+        sub = DMat(dA.t, m, k, dA.ld)
+        ptr = dA.at(r0, c0)
+        C = _dm(np.zeros((m, 90)))
+        lib = load()
+        lw = lib.utv_dgemm_bufsize(m, 90, k)
+        ws = workspace(lw)
+        check(lib.utv_dgemm(b"N", b"N", m, 90, k, 1.0, ptr, sub.ld, dB.ptr, dB.ld, 0.0, C.ptr, C.ld,
+                            ws.data_ptr(), lw, stream_ptr()), "dgemm")
+        ref = big[r0:r0 + m, c0:c0 + k] @ Bm[:k]
+        assert np.abs(C.to_numpy() - ref).max() < 1e-12 * k
+
+
+def test_dgemm_rejects_odd_ld(dv):
+    from paper_2106_13402_b200._lib import load
+    lib = load()
+    st = lib.utv_dgemm(b"N", b"N", 4, 4, 4, 1.0, 0, 5, 0, 4, 0.0, 0, 4, 0, 0, 0)
+    assert st == -8
+
+
+HQR = ["hqr_eye4", "hqr_col34", "hqr_rand100x60", "hqr_rankdef40x24", "hqr_collinear6x3",
+       "hqr_square33"]
+
+
+@pytest.mark.parametrize("name", HQR)
+def test_geqrf_matches_reference_golden(dv, golden, name):
+    g = golden(name)
+    d = _dm(g["A"])
+    Y, T = dv.geqrf(d)
+    scale = max(1.0, np.abs(g["A"]).max())
+    assert np.abs(Y.to_numpy() - g["Y"]).max() <= 1e-12
+    assert np.abs(T.to_numpy() - g["Twy"]).max() <= 1e-12
+    R = d.to_numpy()
+    assert np.abs(R - g["R"]).max() <= 1e-12 * scale
+    assert not np.tril(R, -1).any()
+
+
+@pytest.mark.parametrize("shape", [(500, 256), (2048, 256), (1500, 700), (640, 33), (9000, 64)])
+def test_geqrf_matches_oracle_large(dv, shape):
+    from oracle import utv_oracle as orc
+    m, n = shape
+    rng = np.random.default_rng(m + n)
+    A = rng.standard_normal((m, n))
+    d = _dm(A)
+    Y, T = dv.geqrf(d)
+    y, t, r = orc.householder_qr(A) if m * n <= 600_000 else (None, None, None)
+    Yd, Td, Rd = Y.to_numpy(), T.to_numpy(), d.to_numpy()
+    if y is not None:
+        assert np.abs(Yd - y).max() < 1e-11
+        assert np.abs(Td - t).max() < 1e-11
+        assert np.abs(Rd - r).max() < 1e-11 * np.abs(A).max() * np.sqrt(m)
+    # reconstruction through the compact WY form
+    Q = orc.wy_materialize(Yd, Td, n)
+    assert np.linalg.norm(Q @ Rd[:n] - A) / np.linalg.norm(A) < 1e-14
+    assert np.linalg.norm(Q.T @ Q - np.eye(n)) < 1e-13 * max(m, n)
+
+
+def test_larfb_orgqr_match_reference_golden(dv, golden):
+    g = golden("applyq_50x30")
+    d = _dm(g["A"])
+    Y, T = dv.geqrf(d)
+    for side, trans, key, B in [("L", False, "left", g["BL"]), ("L", True, "left_t", g["BL"]),
+                                ("R", False, "right", g["BR"]), ("R", True, "right_t", g["BR"])]:
+        dB = _dm(B)
+        dv.larfb(side, trans, Y, T, dB)
+        assert np.abs(dB.to_numpy() - g[key]).max() < 1e-13, key
+    assert np.abs(dv.orgqr(Y, T, 50).to_numpy() - g["Q"]).max() < 1e-14
+    assert np.abs(dv.orgqr(Y, T, 30).to_numpy() - g["Q30"]).max() < 1e-14
+
+
+SVD = ["svd_diag321", "svd_rand20", "svd_zero5", "svd_upper64"]
+
+
+@pytest.mark.parametrize("name", SVD)
+def test_gesvj_matches_reference_golden(dv, golden, name):
+    g = golden(name)
+    sig, U, V, st = dv.gesvj(_dm(g["A"]))
+    n = g["A"].shape[0]
+    assert int(st.cpu().item()) > 0
+    s = sig.cpu().numpy()[:n]
+    assert np.abs(s - g["sigma"]).max() <= 1e-13 * max(1.0, g["sigma"].max())
+    # singular vectors are determined to ~eps*||A||/gap (Davis-Kahan); compare
+    # each pair against that bound instead of a flat 1e-12
+    sg = g["sigma"]
+    gap = np.minimum(np.abs(np.diff(sg, prepend=np.inf)), np.abs(np.diff(sg, append=-np.inf)))
+    tol = np.minimum(1.0, 1e-12 + 64 * np.finfo(float).eps * max(sg.max(), 1e-300) / np.maximum(gap, 1e-300))
+    assert np.all(np.abs(U.to_numpy() - g["U"]).max(axis=0) <= tol)
+    assert np.all(np.abs(V.to_numpy() - g["V"]).max(axis=0) <= tol)
+
+
+@pytest.mark.parametrize("n", [1, 2, 17, 128, 200, 256, 384])
+def test_gesvj_random_upper(dv, n):
+    from oracle import utv_oracle as orc
+    rng = np.random.default_rng(n)
+    A = np.triu(rng.standard_normal((n, n)))
+    A[:, :n // 3] *= 1e-4
+    sig, U, V, st = dv.gesvj(_dm(A))
+    assert int(st.cpu().item()) > 0
+    u, s, v = orc.svd_signed(A)
+    sd = sig.cpu().numpy()[:n]
+    assert np.all(np.abs(sd - s) <= 1e-10 * s + 16 * orc.EPS * s.max())
+    Ud, Vd = U.to_numpy(), V.to_numpy()
+    assert np.linalg.norm(Ud.T @ Ud - np.eye(n)) < 1e-12 * n
+    assert np.linalg.norm(Vd.T @ Vd - np.eye(n)) < 1e-12 * n
+    assert np.linalg.norm(Ud @ np.diag(sd) @ Vd.T - A) < 1e-13 * np.linalg.norm(A) * np.sqrt(n)
+    # singular vectors match LAPACK's (sign rule) where the gap is healthy
+    gap = np.minimum(np.abs(np.diff(s, prepend=np.inf)), np.abs(np.diff(s, append=-np.inf)))
+    ok = gap > 1e-3 * s.max()
+    assert np.abs(Vd[:, ok] - v[:, ok]).max() < 1e-9
+
+
+def test_gesvj_rank_deficient_completes_u(dv):
+    rng = np.random.default_rng(3)
+    n = 64
+    A = np.triu(rng.standard_normal((n, n)))
+    A[:, 40:] = 0.0
+    A[40:, :] = 0.0
+    sig, U, V, st = dv.gesvj(_dm(A))
+    Ud = U.to_numpy()
+    assert np.linalg.norm(Ud.T @ Ud - np.eye(n)) < 1e-12 * n
+    assert np.all(sig.cpu().numpy()[40:] == 0.0)
+
+
+@pytest.mark.parametrize("ta,tb", [(True, False), (True, True), (False, True), (False, False)])
+@pytest.mark.parametrize("ra,rb", [(1, 0), (0, 1), (1, 1), (3, 2)])
+def test_dgemm_parity_offsets_all_ops(dv, ta, tb, ra, rb):
+    """Every op combination with odd/even sub-matrix row offsets on both operands."""
+    from paper_2106_13402_b200._lib import check, load, stream_ptr, workspace
+    rng = np.random.default_rng(ra * 10 + rb)
+    m, n, k = 150, 70, 300
+    Abig = rng.standard_normal((400, 400))
+    Bbig = rng.standard_normal((400, 400))
+    A = Abig[ra:ra + (k if ta else m), 2:2 + (m if ta else k)]
+    B = Bbig[rb:rb + (n if tb else k), 5:5 + (k if tb else n)]
+    dA, dB = _dm(Abig), _dm(Bbig)
+    C = _dm(np.zeros((m, n)))
+    lib = load()
+    lw = lib.utv_dgemm_bufsize(m, n, k)
+    ws = workspace(lw)
+    check(lib.utv_dgemm(b"T" if ta else b"N", b"T" if tb else b"N", m, n, k, 1.0, dA.at(ra, 2), dA.ld,
+                        dB.at(rb, 5), dB.ld, 0.0, C.ptr, C.ld, ws.data_ptr(), lw, stream_ptr()), "dgemm")
+    ref = (A.T if ta else A) @ (B.T if tb else B)
+    assert np.abs(C.to_numpy() - ref).max() < 1e-12 * k

@@ -1,0 +1,127 @@
+"""End-to-end GPU parity of the drop-in API (paper_2106_13402_b200) with the
+reference: golden vectors produced by utvkit itself, plus the CPU oracle at
+C1 size (randUTV b=128 q=1 on a 2000^2 geometric-decay matrix).
+
+Tolerances (BASELINE.json north star): diag(T)/diag(R) and the
+Frobenius e_k curve within 1e-10 relative with an absolute floor of
+16*eps*||A||_2 (mixed gate); U/V element-wise max-abs;
+reconstruction and orthogonality at roundoff level.
+"""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from oracle import utv_oracle as orc
+from tests.conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+def _names(prefix):
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, prefix + "*.npz")))
+
+
+def _mixed_ok(x, ref, anorm2, rel=1e-10):
+    return np.all(np.abs(x - ref) <= rel * np.abs(ref) + 16 * orc.EPS * anorm2)
+
+
+@pytest.mark.parametrize("name", _names("rutv_"))
+def test_randutv_basic_matches_reference(golden, name):
+    import paper_2106_13402_b200 as pk
+    g = golden(name)
+    a = g["A"]
+    b, q, seed = int(g["b"]), int(g["q"]), int(g["seed"])
+    f = pk.randutv_basic(a, b, q, pk.RngStream(seed), record_trailing=True)
+    anorm2 = np.linalg.norm(a, 2)
+    assert f.steps_done == int(g["steps"])
+    assert _mixed_ok(np.diag(f.T), np.diag(g["T"]), anorm2)
+    assert _mixed_ok(pk.trailing_fro_curve(f.T), g["efro"], anorm2)
+    m, n = a.shape
+    # Singular vectors are compared where they are determined: columns whose
+    # diag(T) value is above the rank-deficiency noise (1e-8 ||A||_2), and for
+    # tall inputs only the first n columns of U (the rest is a non-unique
+    # orthonormal completion, as with LAPACK).
+    d = np.abs(np.diag(g["T"]))
+    k = int(np.sum(d > 1e-8 * anorm2))
+    assert np.abs(f.U[:, :k] - g["U"][:, :k]).max() < 1e-8
+    assert np.abs(f.V[:, :k] - g["V"][:, :k]).max() < 1e-8
+    assert orc.reconstruction(a, f.U, f.T, f.V) < 1e-13
+    assert orc.orthogonality(f.U) < 1e-13 * m
+    assert orc.orthogonality(f.V) < 1e-13 * n
+    assert np.allclose(f.errors, g["errors"], rtol=1e-8, atol=1e-7 * np.linalg.norm(a))
+    assert np.allclose(f.trailing_fro, g["trailing"], rtol=1e-9, atol=1e-12 * np.linalg.norm(a))
+    # structural zeros (randutv.py:149,154)
+    T = f.T
+    for i in range(f.steps_done - 1):
+        lo, mid = i * b, (i + 1) * b
+        assert not T[mid:, lo:mid].any()
+        blk = T[lo:mid, lo:mid]
+        assert not (blk - np.diag(np.diag(blk))).any()
+
+
+@pytest.mark.parametrize("name", _names("purv_"))
+def test_power_urv_matches_reference(golden, name):
+    import paper_2106_13402_b200 as pk
+    g = golden(name)
+    a = g["A"]
+    q = int(g["q"])
+    if "G" in g:
+        f = pk.power_urv_from_sample(a, q, g["G"])
+    else:
+        f = pk.power_urv(a, q, pk.RngStream(int(g["seed"])))
+    anorm2 = np.linalg.norm(a, 2)
+    assert _mixed_ok(np.diag(f.R), np.diag(g["R"]), anorm2)
+    assert _mixed_ok(pk.trailing_fro_curve(f.R), orc.trailing_fro(g["R"]), anorm2)
+    for got, ref in [(f.Uq.Y, g["Uy"]), (f.Uq.Twy, g["Ut"]), (f.Vq.Y, g["Vy"]), (f.Vq.Twy, g["Vt"])]:
+        assert np.abs(got - ref).max() < 1e-9
+    U, V = f.U, f.V
+    assert orc.reconstruction(a, U, f.R, V) < 1e-13
+    assert orc.orthogonality(U) < 1e-13 * a.shape[0]
+
+
+def test_randutv_c1_against_oracle():
+    """C1: randUTV b=128 q=1 on a 2000x2000 geometric-decay (beta=1e-5) matrix."""
+    import paper_2106_13402_b200 as pk
+    a, d = orc.decay_matrix(2000, 1e-5, seed=7)
+    blocks = orc.randutv_sample_blocks(orc.gaussian_stream(1), 2000, 2000, 128)
+    ref = orc.randutv_basic(a, 128, 1, blocks)
+    f = pk.randutv_basic(a, 128, 1, pk.RngStream(1))
+    anorm2 = d[0]
+    assert _mixed_ok(np.diag(f.T), np.diag(ref["T"]), anorm2)
+    assert _mixed_ok(pk.trailing_fro_curve(f.T), orc.trailing_fro(ref["T"]), anorm2)
+    assert np.abs(f.U - ref["U"]).max() < 1e-8
+    assert np.abs(f.V - ref["V"]).max() < 1e-8
+    assert orc.reconstruction(a, f.U, f.T, f.V) < 1e-13
+    # north-star gate: orthogonality defects agree to 1e-10 (absolute, they are ~1e-13)
+    assert abs(orc.orthogonality(f.U) - orc.orthogonality(ref["U"])) < 1e-10
+    assert abs(orc.orthogonality(f.V) - orc.orthogonality(ref["V"])) < 1e-10
+
+
+def test_power_urv_c2_shape_small_against_oracle():
+    """powerURV q=2 on a Gaussian-decay 768^2 matrix vs the oracle."""
+    import paper_2106_13402_b200 as pk
+    n = 768
+    a, d = orc.decay_matrix(n, 1e-5, seed=20)
+    g = orc.draw_gaussian(orc.gaussian_stream(2), n, n)
+    ref = orc.power_urv(a, 2, g)
+    f = pk.power_urv_from_sample(a, 2, g)
+    assert _mixed_ok(np.diag(f.R), np.diag(ref["R"]), d[0])
+    assert _mixed_ok(pk.trailing_fro_curve(f.R), orc.trailing_fro(ref["R"]), d[0])
+    assert np.abs(f.Vq.Y - ref["Vy"]).max() < 1e-8
+    assert np.abs(f.Uq.Y - ref["Uy"]).max() < 1e-8
+
+
+def test_api_errors_match_reference():
+    import paper_2106_13402_b200 as pk
+    with pytest.raises(pk.DimensionError):
+        pk.randutv_basic(np.ones((3, 5)), 2, 1, pk.RngStream(0))
+    with pytest.raises(ValueError):
+        pk.randutv_basic(np.ones((5, 5)), 0, 1, pk.RngStream(0))
+    with pytest.raises(ValueError):
+        pk.power_urv(np.full((4, 4), np.nan), 1, pk.RngStream(0))
+    with pytest.raises(pk.DimensionError):
+        pk.power_urv_from_sample(np.ones((6, 4)), 1, np.ones((3, 3)))
+    with pytest.raises(pk.DimensionError):
+        pk.hqr_full(np.ones((2, 3)))
