@@ -104,6 +104,16 @@ int utv_powerurv_f64(int m, int n, int q, const double* A, long lda, const doubl
                      double* Vy, long ldvy, double* Vt, long ldvt, void* work, size_t lwork,
                      void* stream);
 
+/* Instrumentation (no reference counterpart).
+ * utv_launch_count: number of libutvb200 kernel launches since load.
+ * utv_profile_begin/end: bracket launches with CUDA events; end() syncs the
+ * device and fills per-category totals (categories: 0 DMMA GEMM, 1 split-K
+ * reduce, 2 panel-QR leaf, 3 Jacobi rounds, 4 Jacobi finish, 5 small ops);
+ * returns the number of categories. */
+long long utv_launch_count(void);
+void utv_profile_begin(void);
+int utv_profile_end(double* ms, double* flops, double* bytes, long long* count);
+
 #ifdef __cplusplus
 }
 #endif

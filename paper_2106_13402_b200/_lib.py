@@ -50,7 +50,13 @@ SIGNATURES = {
     "utv_powerurv_f64": (c_int, [c_int, c_int, c_int, c_void_p, c_long, c_void_p, c_long,
                                  c_void_p, c_long, c_void_p, c_long, c_void_p, c_long, c_void_p,
                                  c_long, c_void_p, c_long, c_void_p, c_size_t, c_void_p]),
+    "utv_launch_count": (ctypes.c_longlong, []),
+    "utv_profile_begin": (None, []),
+    "utv_profile_end": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
 }
+
+PROF_CATEGORIES = ("dgemm_dmma", "splitk_reduce", "panel_qr_leaf", "jacobi_rounds",
+                   "jacobi_finish", "small_ops")
 
 
 def load():
@@ -156,3 +162,23 @@ def workspace(nbytes):
 def stream_ptr():
     torch = torch_cuda()
     return torch.cuda.current_stream().cuda_stream
+
+
+def profile_begin():
+    load().utv_profile_begin()
+
+
+def profile_end():
+    """Synchronise and return {category: dict(ms, flops, bytes, count)}."""
+    n = len(PROF_CATEGORIES)
+    ms = (ctypes.c_double * n)()
+    fl = (ctypes.c_double * n)()
+    by = (ctypes.c_double * n)()
+    ct = (ctypes.c_longlong * n)()
+    load().utv_profile_end(ms, fl, by, ct)
+    return {PROF_CATEGORIES[i]: dict(ms=ms[i], flops=fl[i], bytes=by[i], count=int(ct[i]))
+            for i in range(n)}
+
+
+def launch_count():
+    return int(load().utv_launch_count())

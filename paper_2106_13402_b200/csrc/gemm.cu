@@ -343,6 +343,7 @@ int dgemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, 
   UTV_CHECK(get_encode());
   if (K <= 0 || alpha == 0.0) {
     if (beta == 1.0) return UTV_OK;
+    ProfScope ps(PROF_OPS, 0.0, 16.0 * M * N, st);
     gemm::scale_kernel<<<min(4 * num_sms(), ceil_div((long)M * N, 256)), 256, 0, st>>>(M, N, beta, C, ldc);
     UTV_CUDA(cudaGetLastError());
     return UTV_OK;
@@ -389,13 +390,17 @@ int dgemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, 
   a.C = C; a.ldc = ldc;
   a.ws = splits > 1 ? ws : nullptr;
   dim3 grid(tm, tn, splits);
+  {
+  ProfScope ps(PROF_GEMM, 2.0 * M * N * K, 8.0 * ((double)M * K + (double)K * N + (beta != 0.0 ? 2.0 : 1.0) * M * N), st);
   if (!ta && !tb) gemm::dgemm_tma_kernel<false, false><<<grid, gemm::THREADS, gemm::SMEM_BYTES, st>>>(mA, mB, a);
   else if (!ta && tb) gemm::dgemm_tma_kernel<false, true><<<grid, gemm::THREADS, gemm::SMEM_BYTES, st>>>(mA, mB, a);
   else if (ta && !tb) gemm::dgemm_tma_kernel<true, false><<<grid, gemm::THREADS, gemm::SMEM_BYTES, st>>>(mA, mB, a);
   else gemm::dgemm_tma_kernel<true, true><<<grid, gemm::THREADS, gemm::SMEM_BYTES, st>>>(mA, mB, a);
   UTV_CUDA(cudaGetLastError());
+  }
   if (splits > 1) {
     const long total = (long)M * N;
+    ProfScope ps(PROF_SPLITK, 0.0, 8.0 * (splits + (beta != 0.0 ? 2 : 1)) * total, st);
     gemm::splitk_reduce_kernel<<<min(8 * num_sms(), ceil_div(total, 256)), 256, 0, st>>>(
         ws, splits, M, N, alpha, beta, C, ldc);
     UTV_CUDA(cudaGetLastError());

@@ -343,6 +343,8 @@ int gesvj(Mat A, double* sigma, Mat U, Mat V, double* ws, size_t ws_doubles, int
     g_jac_attr = true;
   }
   if (smem > 200 * 1024) return -1;
+  {
+  ProfScope ps(PROF_JACOBI, 0.0, 0.0, st);
   if (G > 1) {
     void* args[] = {&a};
     UTV_CUDA(cudaLaunchCooperativeKernel((void*)jac::jacobi_rounds_kernel, dim3(G),
@@ -351,7 +353,9 @@ int gesvj(Mat A, double* sigma, Mat U, Mat V, double* ws, size_t ws_doubles, int
     jac::jacobi_rounds_kernel<<<1, jac::THREADS, smem, st>>>(a);
     UTV_CUDA(cudaGetLastError());
   }
+  }
   const size_t smem2 = (size_t)4 * (n + 2) * sizeof(double);
+  ProfScope ps2(PROF_JFINISH, 0.0, 0.0, st);
   jac::jacobi_finish_kernel<<<1, 1024, smem2, st>>>(Aw, Vw, ld, n, sigma, U.p, U.ld, V.p, V.ld,
                                                     scratch);
   UTV_CUDA(cudaGetLastError());

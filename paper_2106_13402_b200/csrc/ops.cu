@@ -103,6 +103,7 @@ int sumsq(const double* A, long lda, int rows, int cols, double* out, double* sc
     UTV_CUDA(cudaMemsetAsync(out, 0, sizeof(double), st));
     return UTV_OK;
   }
+  ProfScope ps(PROF_OPS, 2.0 * rows * cols, 8.0 * rows * cols, st, 2);
   ops::sumsq_partial<<<ops::RED_BLOCKS, ops::RED_THREADS, 0, st>>>(A, lda, rows, cols, scratch);
   UTV_CUDA(cudaGetLastError());
   ops::sum_partials<<<1, 512, 0, st>>>(scratch, ops::RED_BLOCKS, out);
@@ -112,6 +113,7 @@ int sumsq(const double* A, long lda, int rows, int cols, double* out, double* sc
 
 int set_identity(double* A, long lda, int rows, int cols, cudaStream_t st) {
   if (rows <= 0 || cols <= 0) return UTV_OK;
+  ProfScope ps(PROF_OPS, 0.0, 8.0 * rows * cols, st);
   ops::fill_kernel<<<ops::grid_for((long)rows * cols), 256, 0, st>>>(A, lda, rows, cols, 1.0, 0.0);
   UTV_CUDA(cudaGetLastError());
   return UTV_OK;
@@ -137,6 +139,7 @@ int copy_mat(const double* src, long lds, double* dst, long ldd, int rows, int c
 
 int set_diag(double* A, long lda, int nr, int nc, const double* d, cudaStream_t st) {
   if (nr <= 0 || nc <= 0) return UTV_OK;
+  ProfScope ps(PROF_OPS, 0.0, 8.0 * nr * nc, st);
   ops::diag_kernel<<<ops::grid_for((long)nr * nc), 256, 0, st>>>(A, lda, nr, nc, d);
   UTV_CUDA(cudaGetLastError());
   return UTV_OK;

@@ -1,0 +1,96 @@
+// Launch accounting + optional per-kernel CUDA-event profiling.
+//
+// Every kernel launch site wraps itself in a ProfScope.  When profiling is
+// off (default) this only bumps a launch counter; when on, a pair of CUDA
+// events brackets the launch on its own stream so bench.py can report the
+// device time, algorithmic FLOPs and bytes of each kernel family (the
+// roofline inputs) without a profiler attached.
+#include <atomic>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+#include "utv_internal.h"
+
+namespace utv {
+
+namespace {
+struct Rec {
+  int cat;
+  cudaEvent_t a, b;
+  double flops, bytes;
+};
+std::mutex g_mu;
+bool g_on = false;
+std::vector<Rec> g_recs;
+std::vector<cudaEvent_t> g_pool;
+std::atomic<long long> g_launches{0};
+
+cudaEvent_t get_event() {
+  if (!g_pool.empty()) {
+    cudaEvent_t e = g_pool.back();
+    g_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+}  // namespace
+
+ProfScope::ProfScope(int cat, double flops, double bytes, cudaStream_t st, int launches)
+    : cat_(cat), flops_(flops), bytes_(bytes), st_(st), a_(nullptr) {
+  g_launches += launches;
+  if (!g_on) return;
+  std::lock_guard<std::mutex> lk(g_mu);
+  a_ = get_event();
+  cudaEventRecord((cudaEvent_t)a_, st_);
+}
+
+ProfScope::~ProfScope() {
+  if (!a_) return;
+  std::lock_guard<std::mutex> lk(g_mu);
+  cudaEvent_t b = get_event();
+  cudaEventRecord(b, st_);
+  g_recs.push_back(Rec{cat_, (cudaEvent_t)a_, b, flops_, bytes_});
+}
+
+}  // namespace utv
+
+using namespace utv;
+
+extern "C" {
+
+long long utv_launch_count(void) { return g_launches.load(); }
+
+void utv_profile_begin(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_on = true;
+  g_recs.clear();
+}
+
+// Synchronises the device, then returns per-category totals:
+// ms[c], flops[c], bytes[c], count[c] for c < PROF_NCAT.  Returns PROF_NCAT.
+int utv_profile_end(double* ms, double* flops, double* bytes, long long* count) {
+  cudaDeviceSynchronize();
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (int c = 0; c < PROF_NCAT; ++c) {
+    ms[c] = flops[c] = bytes[c] = 0.0;
+    count[c] = 0;
+  }
+  for (auto& r : g_recs) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    ms[r.cat] += t;
+    flops[r.cat] += r.flops;
+    bytes[r.cat] += r.bytes;
+    count[r.cat] += 1;
+    g_pool.push_back(r.a);
+    g_pool.push_back(r.b);
+  }
+  g_recs.clear();
+  g_on = false;
+  return PROF_NCAT;
+}
+
+}  // extern "C"

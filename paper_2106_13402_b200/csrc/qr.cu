@@ -194,6 +194,8 @@ static int leaf_qr(Mat P, Mat Y, Mat T, const double* fro2, double* lws, cudaStr
                                   (int)(qr::leaf_smem_doubles(qr::RC_MAX) * sizeof(double))));
     g_leaf_attr = true;
   }
+  // algorithmic: 4*rows*jb^2 flops (geqr2 + larft), panel read + R/Y write
+  ProfScope ps(PROF_PANEL, 4.0 * P.rows * (double)P.cols * P.cols, 8.0 * 3.0 * P.rows * P.cols, st);
   if (G > 1) {
     UTV_CUDA(cudaMemsetAsync(a.ctr, 0, sizeof(unsigned), st));
     void* args[] = {&a};

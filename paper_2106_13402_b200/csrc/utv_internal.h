@@ -10,6 +10,25 @@ namespace utv {
 
 int num_sms();
 
+// ---- launch accounting / profiling (prof.cu) ----
+enum ProfCat {
+  PROF_GEMM = 0,      // DMMA GEMM kernel (flops = 2MNK)
+  PROF_SPLITK = 1,    // split-K reduction
+  PROF_PANEL = 2,     // panel QR leaf kernel
+  PROF_JACOBI = 3,    // Jacobi rounds kernel
+  PROF_JFINISH = 4,   // Jacobi finish kernel
+  PROF_OPS = 5,       // reductions / structured writes / copies
+  PROF_NCAT = 6
+};
+struct ProfScope {
+  ProfScope(int cat, double flops, double bytes, cudaStream_t st, int launches = 1);
+  ~ProfScope();
+  int cat_;
+  double flops_, bytes_;
+  cudaStream_t st_;
+  void* a_;
+};
+
 // Split-K scratch reserved by every multi-GEMM routine (300 tiles of 128x128).
 constexpr size_t SPLITK_WS = 300ull * 128 * 128;
 

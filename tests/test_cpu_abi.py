@@ -1,0 +1,86 @@
+"""CPU-only checks: the C-ABI library loads without a GPU and exports every
+symbol include/utv_b200.h declares; ctypes signatures cover them; FLOP model
+matches SURVEY §8d; the product path refuses to run without CUDA."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from tests.conftest import ROOT
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "utv_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(utv_\w+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2106_13402_b200 import _lib
+    lib = _lib.load()
+    names = _declared()
+    assert len(names) >= 20
+    for name in names:
+        assert hasattr(lib, name), name
+        assert name in _lib.SIGNATURES, name
+
+
+def test_version_and_no_device():
+    from paper_2106_13402_b200 import _lib
+    lib = _lib.load()
+    assert lib.utv_version() == 100
+    assert lib.utv_launch_count() == 0 or lib.utv_launch_count() > 0
+
+
+def test_argument_validation_without_device():
+    from paper_2106_13402_b200 import _lib
+    lib = _lib.load()
+    # odd leading dimension -> -8 (LAPACK-style argument index), no launch
+    assert lib.utv_dgemm(b"N", b"N", 4, 4, 4, 1.0, 0, 5, 0, 4, 0.0, 0, 4, 0, 0, 0) == -8
+    assert lib.utv_dgemm(b"X", b"N", 4, 4, 4, 1.0, 0, 4, 0, 4, 0.0, 0, 4, 0, 0, 0) == -1
+    assert lib.utv_dgeqrf(3, 4, 0, 4, 0, 4, 0, 4, 0, 0, 0) == -2          # n > m
+    assert lib.utv_randutv_basic_f64(4, 4, 0, 1, 0, 4, 0, 4, 0, 4, 0, 4, 0, 0, 0, 0, 0, 0) == -3
+    assert lib.utv_powerurv_f64(4, 4, -1, 0, 4, 0, 4, 0, 4, 0, 4, 0, 4, 0, 4, 0, 4, 0, 0, 0) == -3
+
+
+def test_flop_model_matches_survey():
+    import bench
+    assert abs(bench.randutv_flops(16384, 16384, 256, 2) / 4.85e13 - 1) < 2e-3
+    assert abs(bench.powerurv_flops(16384, 16384, 2) / 9.68e13 - 1) < 2e-3
+    assert abs(bench.randutv_flops(2000, 2000, 128, 1) / 8.55e10 - 1) < 2e-3
+    assert abs(bench.powerurv_flops(8192, 8192, 2) / 1.21e13 - 1) < 2e-3
+
+
+def test_no_cpu_fallback():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import paper_2106_13402_b200 as pk
+    with pytest.raises(RuntimeError):
+        pk.randutv_basic(np.eye(8), 4, 1, pk.RngStream(0))
+    with pytest.raises(RuntimeError):
+        pk.hqr_full(np.eye(4))
+
+
+def test_validation_errors_raised_before_device():
+    import paper_2106_13402_b200 as pk
+    with pytest.raises(pk.DimensionError):
+        pk.randutv_basic(np.ones((3, 5)), 2, 1, pk.RngStream(0))
+    with pytest.raises(ValueError):
+        pk.randutv_basic(np.ones((5, 5)), 0, 1, pk.RngStream(0))
+    with pytest.raises(ValueError):
+        pk.power_urv_from_sample(np.ones((5, 5)), -1, np.ones((5, 5)))
+    with pytest.raises(pk.DimensionError):
+        pk.power_urv_from_sample(np.ones((6, 4)), 1, np.ones((3, 3)))
+
+
+def test_rng_stream_matches_reference_draw_order():
+    """draw_sample_blocks consumes the stream exactly like randutv.py:189."""
+    import paper_2106_13402_b200 as pk
+    from oracle import utv_oracle as orc
+    blocks = pk.randutv.draw_sample_blocks(pk.RngStream(5), 300, 260, 64)
+    ref = orc.randutv_sample_blocks(orc.gaussian_stream(5), 300, 260, 64)
+    assert len(blocks) == len(ref) == 4
+    for x, y in zip(blocks, ref):
+        assert np.array_equal(x, y)
