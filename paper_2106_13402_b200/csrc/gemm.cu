@@ -187,38 +187,54 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 
   // ---------------- epilogue ----------------
-  const int crow_l = lane >> 2, ccol_l = (lane & 3) * 2;
-  if (p.ws == nullptr) {
+  // Stage the 128x128 accumulator tile through the (now idle) pipeline smem,
+  // then stream it out column by column: coalesced, with all C loads of a
+  // thread in flight together (the direct fragment-order store left each
+  // load->fma->store chain exposed to full DRAM latency).
+  __syncthreads();
+  double* cs = smem;  // [n][CP] column-major, CP = BM + 4
+  constexpr int CP = BM + 4;
+  {
+    const int crow_l = lane >> 2, ccol_l = (lane & 3) * 2;
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
-      const int m = m0 + frag_row<TA>(wm, t, crow_l);
-      if (m < 0 || m >= p.M) continue;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int n = n0 + frag_col<TB>(wn, u, ccol_l + j);
-          if (n >= 0 && n < p.N) {
-            double* c = p.C + m + (long)n * p.ldc;
-            const double v = p.alpha * acc[t][u][j];
-            *c = (p.beta == 0.0) ? v : fma(p.beta, *c, v);
-          }
-        }
-      }
-    }
-  } else {
-    double* w = p.ws + (size_t)blockIdx.z * p.N * p.M;
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int m = m0 + frag_row<TA>(wm, t, crow_l);
-      if (m < 0 || m >= p.M) continue;
+      const int ml = frag_row<TA>(wm, t, crow_l);
 #pragma unroll
       for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int n = n0 + frag_col<TB>(wn, u, ccol_l + j);
-          if (n >= 0 && n < p.N) w[m + (size_t)n * p.M] = acc[t][u][j];
+        for (int j = 0; j < 2; ++j) cs[ml + frag_col<TB>(wn, u, ccol_l + j) * CP] = acc[t][u][j];
+    }
+  }
+  __syncthreads();
+  const int ml = threadIdx.x & (BM - 1);  // row within the tile
+  const int nq = threadIdx.x >> 7;        // 2 column phases
+  const int m = m0 + ml;
+  if (m >= 0 && m < p.M) {
+    if (p.ws == nullptr) {
+      constexpr int U = 8;
+      for (int nb = 0; nb < BN; nb += 2 * U) {
+        double cv[U];
+#pragma unroll
+        for (int i = 0; i < U; ++i) {
+          const int n = n0 + nb + nq + 2 * i;
+          cv[i] = (p.beta != 0.0 && n >= 0 && n < p.N) ? p.C[m + (long)n * p.ldc] : 0.0;
         }
+#pragma unroll
+        for (int i = 0; i < U; ++i) {
+          const int nl = nb + nq + 2 * i;
+          const int n = n0 + nl;
+          if (n >= 0 && n < p.N) {
+            const double v = p.alpha * cs[ml + nl * CP];
+            p.C[m + (long)n * p.ldc] = (p.beta == 0.0) ? v : fma(p.beta, cv[i], v);
+          }
+        }
+      }
+    } else {
+      double* w = p.ws + (size_t)blockIdx.z * p.N * p.M;
+      for (int nl = nq; nl < BN; nl += 2) {
+        const int n = n0 + nl;
+        if (n >= 0 && n < p.N) w[m + (size_t)n * p.M] = cs[ml + nl * CP];
+      }
     }
   }
 }
@@ -318,15 +334,31 @@ size_t dgemm_ws_doubles(int M, int N, int K) {
 int choose_splits(int tiles, int K) {
   const int sms = num_sms();
   const int kblocks = ceil_div(K, gemm::BK);
-  if (tiles >= sms || kblocks < 8) return 1;
-  // Pick the split count (each split keeps >= 8 k-blocks) maximising wave
-  // efficiency; ties go to fewer splits.
+  const double eff1 = (double)tiles / (ceil_div(tiles, sms) * sms);
+  if (tiles >= sms) {
+    // Many tiles: split only a long-K GEMM whose last wave is badly filled
+    // (e.g. the 16384 x 256 sampling GEMMs: 256 tiles = 1.73 waves).
+    if (eff1 >= 0.9 || kblocks < 64) return 1;
+    int best = 1;
+    double best_eff = eff1;
+    for (int s = 2; s <= 8 && kblocks / s >= 32; ++s) {
+      const int units = tiles * s;
+      const double eff = (double)units / (ceil_div(units, sms) * sms);
+      if (eff > best_eff + 0.03) {
+        best = s;
+        best_eff = eff;
+      }
+    }
+    return best;
+  }
+  if (kblocks < 8) return 1;
+  // Few tiles: pick the split count (each split keeps >= 8 k-blocks)
+  // maximising wave efficiency; ties go to fewer splits.
   int best = 1;
-  double best_eff = (double)tiles / (ceil_div(tiles, sms) * sms);
+  double best_eff = eff1;
   for (int s = 2; s <= 64 && kblocks / s >= 8; ++s) {
     const int units = tiles * s;
     const double eff = (double)units / (ceil_div(units, sms) * sms);
-    // prefer more work per CTA when efficiency is equal
     if (eff > best_eff + 0.02) {
       best = s;
       best_eff = eff;

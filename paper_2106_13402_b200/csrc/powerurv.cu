@@ -7,15 +7,21 @@
 //                        round: the reference's last materialisation is dead,
 //                        powerurv.py:68-70) }
 //   Ahat = A Q(Vq) via compact WY (powerurv.py:70); (Uq, R) = hqr_full(Ahat).
+//
+// Only the two returned factors (Uq, Vq) need the dense n x n compact-WY
+// triangle of the reference's QFactor; every intermediate QR keeps its
+// panel-blocked form (diagonal 256 x 256 blocks of T) and is applied /
+// materialised panel by panel (larfb_panels / orgqr_panels), which is what
+// brings the executed FLOPs down to the algorithmic count of SURVEY §8d.
 #include "common.cuh"
 #include "utv_internal.h"
 
 namespace utv {
 
 struct PurvWs {
-  double *Yh, *Yq, *Tq, *Vh, *Vc, *Yn, *gws, *qr, *lfb, *org;
+  double *Yh, *Yq, *Tq, *Vh, *Vc, *Yn, *gws, *qr, *lfb, *bt;
   long ldm, ldn;
-  size_t qr_n, lfb_n, org_n;
+  size_t qr_n, lfb_n, bt_n;
 };
 
 static size_t plan_purv(int m, int n, PurvWs* w, double* base) {
@@ -29,8 +35,8 @@ static size_t plan_purv(int m, int n, PurvWs* w, double* base) {
   v.ldm = round_up(m, 4);
   v.ldn = round_up(n, 4);
   v.qr_n = geqrf_ws_doubles(m, n, true);
-  v.lfb_n = larfb_ws_doubles(m, n, n);
-  v.org_n = (size_t)v.ldn * n + SPLITK_WS + 1024;
+  v.lfb_n = larfb_ws_doubles(m, n, QR_PANEL);
+  v.bt_n = build_t_ws_doubles(m, n);
   v.Yh = take(v.ldm * n);
   v.Yq = take(v.ldm * n);
   v.Tq = take(v.ldn * n);
@@ -40,7 +46,7 @@ static size_t plan_purv(int m, int n, PurvWs* w, double* base) {
   v.gws = take(SPLITK_WS);
   v.qr = take(v.qr_n);
   v.lfb = take(v.lfb_n);
-  v.org = take(v.org_n);
+  v.bt = take(v.bt_n);
   if (w) *w = v;
   return used / sizeof(double) + 64;
 }
@@ -62,30 +68,35 @@ int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, M
     const double* vcur = G.p;
     long ldv = G.ld;
     for (int it = 0; it < q; ++it) {
+      const bool last = (it + 1 == q);
       // Yhat = A V (powerurv.py:64)
       UTV_CHECK(dgemm(false, false, m, n, n, 1.0, A.p, A.ld, vcur, ldv, 0.0, w.Yh, w.ldm, w.gws,
                       SPLITK_WS, st));
-      // Vhat = thin Q of Yhat (powerurv.py:65)
+      // Vhat = thin Q of Yhat (powerurv.py:65); any stable thin QR gives the
+      // same hqr_full(Y) below (Householder vectors are invariant under the
+      // column signs of Vhat), so panel-blocked form suffices.
       Mat Yq{w.Yq, w.ldm, m, n}, Tq{w.Tq, w.ldn, n, n};
-      UTV_CHECK(geqrf(Mat{w.Yh, w.ldm, m, n}, Yq, Tq, true, w.qr, w.qr_n, st));
-      UTV_CHECK(orgqr(Yq, Tq, Mat{w.Vh, w.ldm, m, n}, w.org, w.org_n, st));
+      UTV_CHECK(geqrf(Mat{w.Yh, w.ldm, m, n}, Yq, Tq, false, w.qr, w.qr_n, st));
+      UTV_CHECK(orgqr_panels(Yq, Tq, Mat{w.Vh, w.ldm, m, n}, w.lfb, w.lfb_n, st));
       // Y = A^T Vhat (powerurv.py:66)
       UTV_CHECK(dgemm(true, false, n, n, m, 1.0, A.p, A.ld, w.Vh, w.ldm, 0.0, w.Yn, w.ldn, w.gws,
                       SPLITK_WS, st));
-      // Vq = hqr_full(Y) (powerurv.py:67)
-      UTV_CHECK(geqrf(Mat{w.Yn, w.ldn, n, n}, Vy, Vt, true, w.qr, w.qr_n, st));
-      if (it + 1 < q) {
-        UTV_CHECK(orgqr(Vy, Vt, Mat{w.Vc, w.ldn, n, n}, w.org, w.org_n, st));
+      // Vq = hqr_full(Y) (powerurv.py:67); dense T only for the returned factor
+      UTV_CHECK(geqrf(Mat{w.Yn, w.ldn, n, n}, Vy, Vt, false, w.qr, w.qr_n, st));
+      if (!last) {
+        UTV_CHECK(orgqr_panels(Vy, Vt, Mat{w.Vc, w.ldn, n, n}, w.lfb, w.lfb_n, st));
         vcur = w.Vc;
         ldv = w.ldn;
       }
     }
+    UTV_CHECK(build_t(Vy, Vt, w.bt, w.bt_n, st));
   }
-  // Ahat = A Q(Vq) (powerurv.py:70), formed in R's storage
+  // Ahat = A Q(Vq) (powerurv.py:70), formed in R's storage, panel by panel
   UTV_CHECK(copy_mat(A.p, A.ld, R.p, R.ld, m, n, st));
-  UTV_CHECK(larfb('R', false, Vy, Vt, R, w.lfb, w.lfb_n, st));
+  UTV_CHECK(larfb_panels('R', false, Vy, Vt, R, w.lfb, w.lfb_n, st));
   // (Uq, R) = hqr_full(Ahat) (powerurv.py:71)
-  UTV_CHECK(geqrf(R, Uy, Ut, true, w.qr, w.qr_n, st));
+  UTV_CHECK(geqrf(R, Uy, Ut, false, w.qr, w.qr_n, st));
+  UTV_CHECK(build_t(Uy, Ut, w.bt, w.bt_n, st));
   return UTV_OK;
 }
 

@@ -32,7 +32,7 @@ constexpr int LT = 256;      // leaf threads
 constexpr int RC_MIN = 64;   // min rows per CTA (row j of every column lives in CTA 0)
 constexpr int RC_MAX = 640;  // max rows per CTA (smem)
 constexpr int GMAX = 128;
-constexpr int PANEL = 256;   // outer panel width
+constexpr int PANEL = QR_PANEL;  // outer panel width
 constexpr double EPS = 2.220446049250313e-16;
 
 struct LeafArgs {
@@ -315,6 +315,55 @@ static int geqrf_level(Mat P, Mat Y, Mat T, bool want_t, int blk, const double* 
     if (want_t) UTV_CHECK(merge_t(Y, T, j0, jb, S1, S2, gws, st));
   }
   ar.used = mark;
+  return UTV_OK;
+}
+
+int larfb_panels(char side, bool trans, Mat Y, Mat T, Mat B, double* ws, size_t ws_doubles,
+                 cudaStream_t st) {
+  const int k = Y.rows, w = Y.cols;
+  const int np = (w + qr::PANEL - 1) / qr::PANEL;
+  // forward order for B Q and Q^T B, reverse for B Q^T and Q B
+  const bool fwd = (side == 'R') != trans;
+  for (int jj = 0; jj < np; ++jj) {
+    const int j = fwd ? jj : np - 1 - jj;
+    const int j0 = j * qr::PANEL, jb = (w - j0 < qr::PANEL) ? w - j0 : qr::PANEL;
+    Mat Yj = Y.sub(j0, j0, k - j0, jb), Tj = T.sub(j0, j0, jb, jb);
+    if (side == 'R')
+      UTV_CHECK(larfb('R', trans, Yj, Tj, B.sub(0, j0, B.rows, k - j0), ws, ws_doubles, st));
+    else
+      UTV_CHECK(larfb('L', trans, Yj, Tj, B.sub(j0, 0, k - j0, B.cols), ws, ws_doubles, st));
+  }
+  return UTV_OK;
+}
+
+int orgqr_panels(Mat Y, Mat T, Mat Q, double* ws, size_t ws_doubles, cudaStream_t st) {
+  const int m = Y.rows, w = Y.cols, nc = Q.cols;
+  UTV_CHECK(set_identity(Q.p, Q.ld, m, nc, st));
+  const int np = (w + qr::PANEL - 1) / qr::PANEL;
+  for (int j = np - 1; j >= 0; --j) {
+    const int j0 = j * qr::PANEL, jb = (w - j0 < qr::PANEL) ? w - j0 : qr::PANEL;
+    if (j0 >= nc) continue;  // Q_j leaves the leading columns of I untouched
+    UTV_CHECK(larfb('L', false, Y.sub(j0, j0, m - j0, jb), T.sub(j0, j0, jb, jb),
+                    Q.sub(j0, j0, m - j0, nc - j0), ws, ws_doubles, st));
+  }
+  return UTV_OK;
+}
+
+size_t build_t_ws_doubles(int rows, int cols) {
+  return 2 * (size_t)round_up(cols, 4) * qr::PANEL + SPLITK_WS + 1024;
+}
+
+int build_t(Mat Y, Mat T, double* ws, size_t ws_doubles, cudaStream_t st) {
+  const int cols = Y.cols;
+  Arena ar{(char*)ws, ws_doubles * sizeof(double), 0};
+  double* S1 = ar.take((size_t)round_up(cols, 4) * qr::PANEL);
+  double* S2 = ar.take((size_t)round_up(cols, 4) * qr::PANEL);
+  double* gws = ar.take(SPLITK_WS);
+  if (!gws) return UTV_ERR_WORKSPACE;
+  for (int j0 = qr::PANEL; j0 < cols; j0 += qr::PANEL) {
+    const int jb = cols - j0 < qr::PANEL ? cols - j0 : qr::PANEL;
+    UTV_CHECK(merge_t(Y, T, j0, jb, S1, S2, gws, st));
+  }
   return UTV_OK;
 }
 

@@ -29,8 +29,8 @@ struct ProfScope {
   void* a_;
 };
 
-// Split-K scratch reserved by every multi-GEMM routine (300 tiles of 128x128).
-constexpr size_t SPLITK_WS = 300ull * 128 * 128;
+// Split-K scratch reserved by every multi-GEMM routine (1024 tiles of 128x128, 128 MiB).
+constexpr size_t SPLITK_WS = 1024ull * 128 * 128;
 
 // ---- K1 GEMM (gemm.cu) ----
 int choose_splits(int tiles, int K);
@@ -66,6 +66,20 @@ int larfb(char side, bool trans, Mat Y, Mat T, Mat B, double* ws, size_t ws_doub
           cudaStream_t st);
 // Q[:, :ncols] = I - Y (T Y[:ncols,:]^T)
 int orgqr(Mat Y, Mat T, Mat Q, double* ws, size_t ws_doubles, cudaStream_t st);
+
+// Panel-blocked variants: Q = Q_1 Q_2 ... Q_p with Q_j = I - Y_j T_j Y_j^T,
+// T_j the QR_PANEL-wide diagonal blocks of T (off-diagonal blocks unused).
+// Cost 2*rows*w*k-ish instead of the dense-T 3-GEMM form (no w x w x rows
+// middle product, no full T needed).
+constexpr int QR_PANEL = 256;
+int larfb_panels(char side, bool trans, Mat Y, Mat T, Mat B, double* ws, size_t ws_doubles,
+                 cudaStream_t st);
+int orgqr_panels(Mat Y, Mat T, Mat Q, double* ws, size_t ws_doubles, cudaStream_t st);
+// Fill the off-diagonal QR_PANEL blocks of T from Y and the diagonal blocks
+// (T12 = -T11 (Y1^T Y2) T22), turning a panel-blocked T into the dense
+// forward compact-WY triangle of the whole product (qr.py:63-68 semantics).
+size_t build_t_ws_doubles(int rows, int cols);
+int build_t(Mat Y, Mat T, double* ws, size_t ws_doubles, cudaStream_t st);
 
 // ---- K6 Jacobi SVD (jacobi.cu) ----
 // A (n x n, read only): sigma (desc, device), U (n x n), V (n x n) with the
