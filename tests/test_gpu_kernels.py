@@ -135,7 +135,10 @@ def test_gesvj_matches_reference_golden(dv, golden, name):
     sg = g["sigma"]
     gap = np.minimum(np.abs(np.diff(sg, prepend=np.inf)), np.abs(np.diff(sg, append=-np.inf)))
     tol = np.minimum(2.0, 1e-12 + 64 * np.finfo(float).eps * max(sg.max(), 1e-300) / np.maximum(gap, 1e-300))
-    assert np.all(np.abs(U.to_numpy() - g["U"]).max(axis=0) <= tol)
+    # U = A V / sigma: a column whose sigma sits at the roundoff floor
+    # (svd_upper64: sigma_64 = 4e-16 * sigma_1) is undetermined to O(1)
+    tol_u = np.minimum(2.0, tol + 64 * np.finfo(float).eps * max(sg.max(), 1e-300) / np.maximum(sg, 1e-300))
+    assert np.all(np.abs(U.to_numpy() - g["U"]).max(axis=0) <= tol_u)
     assert np.all(np.abs(V.to_numpy() - g["V"]).max(axis=0) <= tol)
 
 
