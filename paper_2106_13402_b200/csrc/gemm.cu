@@ -8,9 +8,15 @@
 // (randutv.py:152-156,167-172).
 //
 // Design (sm_100a):
-//  * CTA tile 128x128x16, 8 DMMA warps (2x4, warp tile 64x32, 252 regs);
-//    thread 0 also drives TMA through a STAGES-deep full/empty mbarrier ring
-//    of 128B-swizzled smem tiles.
+//  * CTA tile 128x128x16, 8 DMMA warps (2x4, warp tile 64x32, ~255 regs),
+//    persistent: min(tiles, 148) CTAs walk the tile list.  Thread 0 also
+//    drives TMA through a full/empty mbarrier ring of 128B-swizzled smem
+//    tiles, running STAGES-1 k-blocks ahead across tile boundaries so the
+//    next tile's operands land while the current epilogue runs.
+//  * beta != 0: the C tile is TMA-prefetched into a 128 KB smem buffer
+//    during the main loop (3-stage ring); beta == 0: 6-stage ring.  The
+//    epilogue stores from the accumulator fragments directly (every warp
+//    store fills whole 32 B sectors), so no DRAM round trip is exposed.
 //  * mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4). tcgen05 has no f64 kind.
 //  * Fragment rows/cols are mapped onto the 128B-swizzled tiles with a
 //    permutation that makes every 64-bit fragment load bank-conflict free
@@ -30,19 +36,29 @@
 namespace utv {
 
 namespace gemm {
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 5;
+constexpr int BM = 128, BN = 128, BK = 16;
 constexpr int NCW = 8;                   // consumer warps
-constexpr int THREADS = NCW * 32;  // thread 0 also issues TMA
+constexpr int THREADS = NCW * 32;        // thread 0 also issues TMA
 constexpr int A_ST = BM * BK;            // doubles per stage
 constexpr int B_ST = BN * BK;
 constexpr uint32_t STAGE_BYTES = (A_ST + B_ST) * 8;
-constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 + 2 * STAGES * 8 + 64;
+constexpr uint32_t C_BYTES = BM * BN * 8;
+// Ring depth: 6 stages when the tile needs no C input; 3 stages + a 128 KB
+// smem C tile (TMA-prefetched during the main loop) when beta != 0.
+template <bool HASC>
+struct Cfg {
+  static constexpr int STAGES = HASC ? 3 : 6;
+  static constexpr size_t SMEM =
+      (size_t)STAGES * STAGE_BYTES + (HASC ? C_BYTES : 0) + 1024 + (2 * STAGES + 2) * 8 + 64;
+};
 
 struct Args {
   int M, N, K;
   int a_sh, b_sh;    // M/N-origin shift of A_N / B_T tiles (0 or 1), see DESIGN.md
   int k_sh;          // K-origin shift: logical k = k' - k_sh
+  int c_sh;          // row shift of the C tensor map (HASC only)
   int k_split;       // k' elements per split (multiple of BK)
+  int tm, tn, tiles; // tile grid (tiles = tm * tn * splits)
   double alpha, beta;
   double* C;
   long ldc;
@@ -81,160 +97,188 @@ __device__ __forceinline__ int frag_col(int wn, int u, int c) {
   return nblk * 16 + (u & 1) * 4 + (c & 1) + ((c >> 1) & 1) * 8 + (c >> 2) * 2;
 }
 
-template <bool TA, bool TB>
+struct TileCoord {
+  int mc, nc, z;
+};
+__device__ __forceinline__ TileCoord tile_of(const Args& p, int t) {
+  const int per = p.tm * p.tn;
+  TileCoord c;
+  c.z = t / per;
+  const int r = t - c.z * per;
+  c.nc = (r / p.tm) * BN;
+  c.mc = (r % p.tm) * BM;
+  return c;
+}
+
+// Persistent DMMA GEMM.  Each CTA walks tiles blockIdx.x, +gridDim.x, ...
+// Thread 0 is the TMA producer; its cursor runs STAGES-1 k-blocks ahead of
+// the consumers across tile boundaries, so the next tile's operands stream
+// in while the current tile's epilogue runs.  The epilogue stores straight
+// from the accumulator fragments (32B-sector-complete, fire and forget);
+// when beta != 0 the C tile was TMA-prefetched into smem during the main
+// loop, so no DRAM round trip is exposed.
+template <bool TA, bool TB, bool HASC>
 __global__ void __launch_bounds__(THREADS, 1)
     dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA,
-                     const __grid_constant__ CUtensorMap tmB, const Args p) {
+                     const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmC, const Args p) {
+  constexpr int STAGES = Cfg<HASC>::STAGES;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   double* smem = (double*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   double* sA = smem;
   double* sB = smem + STAGES * A_ST;
-  uint64_t* bars = (uint64_t*)(sB + STAGES * B_ST);
+  double* sC = sB + STAGES * B_ST;                       // HASC only (1024B aligned)
+  uint64_t* bars = (uint64_t*)(sC + (HASC ? BM * BN : 0));
   const uint32_t full0 = smem_u32(bars);
   const uint32_t empty0 = smem_u32(bars + STAGES);
+  const uint32_t cfull = smem_u32(bars + 2 * STAGES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // TMA box origins (always 16B aligned) and the logical origin of the tile.
-  const int mc = blockIdx.x * BM, nc = blockIdx.y * BN;
-  const int m0 = mc - (TA ? 0 : p.a_sh), n0 = nc - (TB ? p.b_sh : 0);
-  const int kb = blockIdx.z * p.k_split;
-  const int ke = min(p.K + p.k_sh, kb + p.k_split);
-  const int nk = (ke - kb + BK - 1) / BK;
+  const int ktot = p.K + p.k_sh;
+  auto nk_of = [&](int z) {
+    const int kb = z * p.k_split;
+    const int ke = min(ktot, kb + p.k_split);
+    return (ke - kb + BK - 1) / BK;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, NCW);
     }
+    mbar_init(cfull, 1);
     fence_barrier_init();
   }
   __syncthreads();
 
-  // Thread 0 doubles as the TMA producer: it keeps STAGES-1 k-blocks in
-  // flight ahead of the consumers (refilling a slot once all 8 warps have
-  // released it through the `empty` mbarrier).
-  auto produce = [&](int it) {
-    const int s = it % STAGES;
-    if (it >= STAGES) mbar_wait(empty0 + 8 * s, ((it / STAGES) & 1) ^ 1);
+  // ---- producer state (thread 0 only) ----
+  int ptile = blockIdx.x, pit = 0, pnk = 0;
+  long pg = 0;  // global produced k-block count
+  TileCoord pc{};
+  if (threadIdx.x == 0 && ptile < p.tiles) {
+    pc = tile_of(p, ptile);
+    pnk = nk_of(pc.z);
+  }
+  auto produce_one = [&]() {
+    const int s = (int)(pg % STAGES);
+    if (pg >= STAGES) mbar_wait(empty0 + 8 * s, (uint32_t)(((pg / STAGES) & 1) ^ 1));
     const uint32_t fb = full0 + 8 * s;
     mbar_arrive_expect_tx(fb, STAGE_BYTES);
-    const int k = kb + it * BK;       // k' (even): K-major operands load at k', others at k'-k_sh
+    const int k = pc.z * p.k_split + pit * BK;  // k' (even)
     const uint32_t dA = smem_u32(sA + s * A_ST), dB = smem_u32(sB + s * B_ST);
     if (TA) {
-      tma_load_2d(dA, &tmA, fb, k, mc);
+      tma_load_2d(dA, &tmA, fb, k, pc.mc);
     } else {
 #pragma unroll
-      for (int i = 0; i < BM / 16; ++i) tma_load_2d(dA + i * 2048, &tmA, fb, mc + 16 * i, k - p.k_sh);
+      for (int i = 0; i < BM / 16; ++i) tma_load_2d(dA + i * 2048, &tmA, fb, pc.mc + 16 * i, k - p.k_sh);
     }
     if (!TB) {
-      tma_load_2d(dB, &tmB, fb, k, nc);
+      tma_load_2d(dB, &tmB, fb, k, pc.nc);
     } else {
 #pragma unroll
-      for (int i = 0; i < BN / 16; ++i) tma_load_2d(dB + i * 2048, &tmB, fb, nc + 16 * i, k - p.k_sh);
+      for (int i = 0; i < BN / 16; ++i) tma_load_2d(dB + i * 2048, &tmB, fb, pc.nc + 16 * i, k - p.k_sh);
     }
+    ++pg;
+    if (++pit == pnk) {
+      pit = 0;
+      ptile += gridDim.x;
+      if (ptile < p.tiles) {
+        pc = tile_of(p, ptile);
+        pnk = nk_of(pc.z);
+      }
+    }
+  };
+  auto load_c = [&](int t) {
+    const TileCoord c = tile_of(p, t);
+    const int m0 = c.mc - (TA ? 0 : p.a_sh), n0 = c.nc - (TB ? p.b_sh : 0);
+    mbar_arrive_expect_tx(cfull, C_BYTES);
+#pragma unroll
+    for (int i = 0; i < BM / 16; ++i)
+      tma_load_2d(smem_u32(sC + i * 16 * BN), &tmC, cfull, m0 + p.c_sh + 16 * i, n0);
   };
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    for (int it = 0; it < min(nk, STAGES - 1); ++it) produce(it);
+    if (HASC && blockIdx.x < p.tiles) load_c(blockIdx.x);
+    for (int i = 0; i < STAGES - 1 && ptile < p.tiles; ++i) produce_one();
   }
 
-  // ---------------- DMMA consumers ----------------
   const int wm = warp & 1, wn = warp >> 1;
   const int fr = lane >> 2, fk = lane & 3;
-  double acc[8][4][2];
-#pragma unroll
-  for (int t = 0; t < 8; ++t)
-#pragma unroll
-    for (int u = 0; u < 4; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
-
-  // Per-thread fragment offsets (k-independent parts are folded at use).
   int arow[8], bcol[4];
 #pragma unroll
   for (int t = 0; t < 8; ++t) arow[t] = frag_row<TA>(wm, t, fr);
 #pragma unroll
   for (int u = 0; u < 4; ++u) bcol[u] = frag_col<TB>(wn, u, fr);
 
-  const bool zero_k0 = (p.k_sh != 0) && (blockIdx.z == 0);
-  for (int it = 0; it < nk; ++it) {
-    if (threadIdx.x == 0 && it + STAGES - 1 < nk) produce(it + STAGES - 1);
-    __syncwarp();
-    const int s = it % STAGES;
-    mbar_wait(full0 + 8 * s, (it / STAGES) & 1);
-    const double* a = sA + s * A_ST;
-    const double* b = sB + s * B_ST;
+  long g = 0;   // global consumed k-block count
+  int local = 0;
+  for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x, ++local) {
+    const TileCoord tc = tile_of(p, tile);
+    const int nk = nk_of(tc.z);
+    double acc[8][4][2];
 #pragma unroll
-    for (int kk = 0; kk < BK / 4; ++kk) {
-      const int k = kk * 4 + fk;
-      double af[8], bf[4];
+    for (int t = 0; t < 8; ++t)
 #pragma unroll
-      for (int t = 0; t < 8; ++t) af[t] = a[a_off_of<TA>(k, arow[t])];
-      // k' = 0 is the logical row k = -1 when the K origin is shifted: when
-      // both operands carry real data there (TN), zero it in registers.
-      if (zero_k0 && it == 0 && kk == 0 && fk == 0) {
-#pragma unroll
-        for (int t = 0; t < 8; ++t) af[t] = 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) bf[u] = b[b_off_of<TB>(k, bcol[u])];
-#pragma unroll
-      for (int t = 0; t < 8; ++t)
-#pragma unroll
-        for (int u = 0; u < 4; ++u) dmma884(acc[t][u][0], acc[t][u][1], af[t], bf[u]);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty0 + 8 * s);
-  }
+      for (int u = 0; u < 4; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
 
-  // ---------------- epilogue ----------------
-  // Stage the 128x128 accumulator tile through the (now idle) pipeline smem,
-  // then stream it out column by column: coalesced, with all C loads of a
-  // thread in flight together (the direct fragment-order store left each
-  // load->fma->store chain exposed to full DRAM latency).
-  __syncthreads();
-  double* cs = smem;  // [n][CP] column-major, CP = BM + 4
-  constexpr int CP = BM + 4;
-  {
-    const int crow_l = lane >> 2, ccol_l = (lane & 3) * 2;
+    const bool zero_k0 = (p.k_sh != 0) && (tc.z == 0);
+    for (int it = 0; it < nk; ++it, ++g) {
+      if (threadIdx.x == 0 && pg < g + STAGES && ptile < p.tiles) produce_one();
+      __syncwarp();
+      const int s = (int)(g % STAGES);
+      mbar_wait(full0 + 8 * s, (uint32_t)((g / STAGES) & 1));
+      const double* a = sA + s * A_ST;
+      const double* b = sB + s * B_ST;
+#pragma unroll
+      for (int kk = 0; kk < BK / 4; ++kk) {
+        const int k = kk * 4 + fk;
+        double af[8], bf[4];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) af[t] = a[a_off_of<TA>(k, arow[t])];
+        // k' = 0 is the logical row k = -1 when the K origin is shifted: when
+        // both operands carry real data there (TN), zero it in registers.
+        if (zero_k0 && it == 0 && kk == 0 && fk == 0) {
+#pragma unroll
+          for (int t = 0; t < 8; ++t) af[t] = 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) bf[u] = b[b_off_of<TB>(k, bcol[u])];
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) dmma884(acc[t][u][0], acc[t][u][1], af[t], bf[u]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8 * s);
+    }
+
+    // ---------------- epilogue (straight from the fragments) ----------------
+    const int m0 = tc.mc - (TA ? 0 : p.a_sh), n0 = tc.nc - (TB ? p.b_sh : 0);
+    if (HASC) mbar_wait(cfull, (uint32_t)(local & 1));
+    double* w = p.ws ? p.ws + (size_t)tc.z * p.N * p.M : nullptr;
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
-      const int ml = frag_row<TA>(wm, t, crow_l);
+      const int ml = frag_row<TA>(wm, t, fr);
+      const int m = m0 + ml;
+      const bool mok = (m >= 0 && m < p.M);
 #pragma unroll
       for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) cs[ml + frag_col<TB>(wn, u, ccol_l + j) * CP] = acc[t][u][j];
-    }
-  }
-  __syncthreads();
-  const int ml = threadIdx.x & (BM - 1);  // row within the tile
-  const int nq = threadIdx.x >> 7;        // 2 column phases
-  const int m = m0 + ml;
-  if (m >= 0 && m < p.M) {
-    if (p.ws == nullptr) {
-      constexpr int U = 8;
-      for (int nb = 0; nb < BN; nb += 2 * U) {
-        double cv[U];
-#pragma unroll
-        for (int i = 0; i < U; ++i) {
-          const int n = n0 + nb + nq + 2 * i;
-          cv[i] = (p.beta != 0.0 && n >= 0 && n < p.N) ? p.C[m + (long)n * p.ldc] : 0.0;
-        }
-#pragma unroll
-        for (int i = 0; i < U; ++i) {
-          const int nl = nb + nq + 2 * i;
+        for (int j = 0; j < 2; ++j) {
+          const int nl = frag_col<TB>(wn, u, 2 * fk + j);
           const int n = n0 + nl;
-          if (n >= 0 && n < p.N) {
-            const double v = p.alpha * cs[ml + nl * CP];
-            p.C[m + (long)n * p.ldc] = (p.beta == 0.0) ? v : fma(p.beta, cv[i], v);
+          double v = p.alpha * acc[t][u][j];
+          if (HASC) v = fma(p.beta, sC[swz((ml >> 4) * BN + nl, ml & 15)], v);
+          if (mok && n >= 0 && n < p.N) {
+            if (w) w[m + (size_t)n * p.M] = acc[t][u][j];
+            else p.C[m + (long)n * p.ldc] = v;
           }
         }
-      }
-    } else {
-      double* w = p.ws + (size_t)blockIdx.z * p.N * p.M;
-      for (int nl = nq; nl < BN; nl += 2) {
-        const int n = n0 + nl;
-        if (n >= 0 && n < p.N) w[m + (size_t)n * p.M] = cs[ml + nl * CP];
-      }
+    }
+    if (HASC) {
+      __syncthreads();  // every warp is done with sC
+      if (threadIdx.x == 0 && tile + (int)gridDim.x < p.tiles) load_c(tile + gridDim.x);
     }
   }
 }
@@ -284,9 +328,12 @@ static int get_encode() {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    for (auto f : {gemm::dgemm_tma_kernel<false, false>, gemm::dgemm_tma_kernel<false, true>,
-                   gemm::dgemm_tma_kernel<true, false>, gemm::dgemm_tma_kernel<true, true>})
-      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm::SMEM_BYTES);
+    for (auto f : {gemm::dgemm_tma_kernel<false, false, false>, gemm::dgemm_tma_kernel<false, true, false>,
+                   gemm::dgemm_tma_kernel<true, false, false>, gemm::dgemm_tma_kernel<true, true, false>})
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm::Cfg<false>::SMEM);
+    for (auto f : {gemm::dgemm_tma_kernel<false, false, true>, gemm::dgemm_tma_kernel<false, true, true>,
+                   gemm::dgemm_tma_kernel<true, false, true>, gemm::dgemm_tma_kernel<true, true, true>})
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm::Cfg<true>::SMEM);
   });
   return g_encode ? UTV_OK : UTV_ERR_CUDA;
 }
@@ -414,29 +461,60 @@ int dgemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, 
   int kper = (int)round_up(ceil_div(Kp, splits), gemm::BK);
   splits = ceil_div(Kp, kper);
 
+  // beta != 0 without split-K: the C tile is TMA-prefetched; its map must
+  // share the A tile's row parity (always true for even offsets).
+  bool hasc = (beta != 0.0) && splits == 1;
+  CUtensorMap mC = mA;
+  int c_sh = 0;
+  if (hasc) {
+    UTV_CHECK(make_map(&mC, C, M, N, ldc, 16, gemm::BN, &c_sh));
+    if (c_sh != a_sh) hasc = false;
+  }
+  // beta != 0 with a C map of the wrong parity (odd offsets only): route
+  // through the split-K workspace path (one split) + the reduce kernel.
+  double* ctmp = nullptr;
+  if (beta != 0.0 && splits == 1 && !hasc) {
+    if (ws == nullptr || ws_doubles < (size_t)M * N) {
+      UTV_CUDA(cudaMallocAsync((void**)&ctmp, sizeof(double) * (size_t)M * N, st));
+      ws = ctmp;
+    }
+  }
+  const bool use_ws = splits > 1 || (beta != 0.0 && !hasc);
+
   gemm::Args a;
   a.M = M; a.N = N; a.K = K;
-  a.a_sh = a_sh; a.b_sh = b_sh; a.k_sh = k_sh;
+  a.a_sh = a_sh; a.b_sh = b_sh; a.k_sh = k_sh; a.c_sh = c_sh;
   a.k_split = kper;
+  a.tm = tm; a.tn = tn; a.tiles = tm * tn * splits;
   a.alpha = alpha; a.beta = beta;
   a.C = C; a.ldc = ldc;
-  a.ws = splits > 1 ? ws : nullptr;
-  dim3 grid(tm, tn, splits);
+  a.ws = use_ws ? ws : nullptr;
+  const int grid = a.tiles < num_sms() ? a.tiles : num_sms();
   {
   ProfScope ps(PROF_GEMM, 2.0 * M * N * K, 8.0 * ((double)M * K + (double)K * N + (beta != 0.0 ? 2.0 : 1.0) * M * N), st);
-  if (!ta && !tb) gemm::dgemm_tma_kernel<false, false><<<grid, gemm::THREADS, gemm::SMEM_BYTES, st>>>(mA, mB, a);
-  else if (!ta && tb) gemm::dgemm_tma_kernel<false, true><<<grid, gemm::THREADS, gemm::SMEM_BYTES, st>>>(mA, mB, a);
-  else if (ta && !tb) gemm::dgemm_tma_kernel<true, false><<<grid, gemm::THREADS, gemm::SMEM_BYTES, st>>>(mA, mB, a);
-  else gemm::dgemm_tma_kernel<true, true><<<grid, gemm::THREADS, gemm::SMEM_BYTES, st>>>(mA, mB, a);
+  if (hasc) {
+    const size_t sm = gemm::Cfg<true>::SMEM;
+    if (!ta && !tb) gemm::dgemm_tma_kernel<false, false, true><<<grid, gemm::THREADS, sm, st>>>(mA, mB, mC, a);
+    else if (!ta && tb) gemm::dgemm_tma_kernel<false, true, true><<<grid, gemm::THREADS, sm, st>>>(mA, mB, mC, a);
+    else if (ta && !tb) gemm::dgemm_tma_kernel<true, false, true><<<grid, gemm::THREADS, sm, st>>>(mA, mB, mC, a);
+    else gemm::dgemm_tma_kernel<true, true, true><<<grid, gemm::THREADS, sm, st>>>(mA, mB, mC, a);
+  } else {
+    const size_t sm = gemm::Cfg<false>::SMEM;
+    if (!ta && !tb) gemm::dgemm_tma_kernel<false, false, false><<<grid, gemm::THREADS, sm, st>>>(mA, mB, mC, a);
+    else if (!ta && tb) gemm::dgemm_tma_kernel<false, true, false><<<grid, gemm::THREADS, sm, st>>>(mA, mB, mC, a);
+    else if (ta && !tb) gemm::dgemm_tma_kernel<true, false, false><<<grid, gemm::THREADS, sm, st>>>(mA, mB, mC, a);
+    else gemm::dgemm_tma_kernel<true, true, false><<<grid, gemm::THREADS, sm, st>>>(mA, mB, mC, a);
+  }
   UTV_CUDA(cudaGetLastError());
   }
-  if (splits > 1) {
+  if (use_ws) {
     const long total = (long)M * N;
     ProfScope ps(PROF_SPLITK, 0.0, 8.0 * (splits + (beta != 0.0 ? 2 : 1)) * total, st);
     gemm::splitk_reduce_kernel<<<min(8 * num_sms(), ceil_div(total, 256)), 256, 0, st>>>(
         ws, splits, M, N, alpha, beta, C, ldc);
     UTV_CUDA(cudaGetLastError());
   }
+  if (ctmp) UTV_CUDA(cudaFreeAsync(ctmp, st));
   if (tmp) UTV_CUDA(cudaFreeAsync(tmp, st));
   return UTV_OK;
 }

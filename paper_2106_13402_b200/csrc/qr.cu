@@ -376,7 +376,10 @@ int geqrf(Mat P, Mat Y, Mat Tw, bool want_t, double* ws, size_t ws_doubles, cuda
   UTV_CHECK(sumsq(P.p, P.ld, P.rows, P.cols, fro2, red, st));
   UTV_CHECK(set_zero(Tw.p, Tw.ld, P.cols, P.cols, st));
   const int blk = P.cols > qr::PANEL ? qr::PANEL : qr::NB;
-  return geqrf_level(P, Y, Tw, want_t, blk, fro2, ar, st);
+  // want_t == false still delivers complete QR_PANEL-wide diagonal blocks of
+  // T (what larfb_panels / orgqr_panels / build_t consume): a single-panel
+  // QR therefore always merges its 32-wide leaf triangles.
+  return geqrf_level(P, Y, Tw, want_t || blk == qr::NB, blk, fro2, ar, st);
 }
 
 }  // namespace utv
