@@ -57,6 +57,7 @@ struct Args {
   int a_sh, b_sh;    // M/N-origin shift of A_N / B_T tiles (0 or 1), see DESIGN.md
   int k_sh;          // K-origin shift: logical k = k' - k_sh
   int c_sh;          // row shift of the C tensor map (HASC only)
+  int a3d, b3d;      // N-major operand mapped as a 3-D {16, K, blocks} tensor (1 TMA per stage)
   int k_split;       // k' elements per split (multiple of BK)
   int tm, tn, tiles; // tile grid (tiles = tm * tn * splits)
   double alpha, beta;
@@ -124,7 +125,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                      const __grid_constant__ CUtensorMap tmC, const Args p) {
   constexpr int STAGES = Cfg<HASC>::STAGES;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  double* smem = (double*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // 1024-byte alignment (128B swizzle atoms) by offsetting the shared pointer
+  // itself: a round trip through uintptr_t would turn every operand load
+  // into a generic 64-bit LD instead of LDS.
+  double* smem = (double*)(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   double* sA = smem;
   double* sB = smem + STAGES * A_ST;
   double* sC = sB + STAGES * B_ST;                       // HASC only (1024B aligned)
@@ -168,12 +172,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t dA = smem_u32(sA + s * A_ST), dB = smem_u32(sB + s * B_ST);
     if (TA) {
       tma_load_2d(dA, &tmA, fb, k, pc.mc);
+    } else if (p.a3d) {
+      tma_load_3d(dA, &tmA, fb, 0, k - p.k_sh, pc.mc >> 4);
     } else {
 #pragma unroll
       for (int i = 0; i < BM / 16; ++i) tma_load_2d(dA + i * 2048, &tmA, fb, pc.mc + 16 * i, k - p.k_sh);
     }
     if (!TB) {
       tma_load_2d(dB, &tmB, fb, k, pc.nc);
+    } else if (p.b3d) {
+      tma_load_3d(dB, &tmB, fb, 0, k - p.k_sh, pc.nc >> 4);
     } else {
 #pragma unroll
       for (int i = 0; i < BN / 16; ++i) tma_load_2d(dB + i * 2048, &tmB, fb, pc.nc + 16 * i, k - p.k_sh);
@@ -314,6 +322,8 @@ __global__ void scale_kernel(int M, int N, double beta, double* C, long ldc) {
 // Host side
 // ---------------------------------------------------------------------------
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+typedef CUresult (*PFN_memRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+static PFN_memRange g_range = nullptr;
 static std::once_flag g_encode_once;
 static int g_num_sms = 0;
 
@@ -325,6 +335,10 @@ static int get_encode() {
             cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
       g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    void* fr = nullptr;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_range = (PFN_memRange)fr;
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
@@ -369,6 +383,32 @@ static int make_map(CUtensorMap* map, const double* p, long rows, long cols, lon
   }
   *shift = sh;
   return UTV_OK;
+}
+
+// 3-D view {16 rows, cols, ceil((rows+sh)/16) row blocks} of an N-major
+// operand, so one TMA box {16, 16, 8} moves a whole 128 x 16 tile.  Rows past
+// `rows` in the last block are READ (not zero-filled); they only feed output
+// rows/columns that are never stored, so the map is used only when that
+// over-read stays inside the pointer's allocation (cuMemGetAddressRange).
+// Returns false (caller keeps the 2-D map) otherwise.
+static bool make_map3d(CUtensorMap* map, const double* p, long rows, long cols, long ld, int sh) {
+  if (!g_range || cols <= 0) return false;
+  const double* base = p - sh;
+  const long nblk = (rows + sh + 15) / 16;
+  CUdeviceptr abase = 0;
+  size_t asize = 0;
+  if (g_range(&abase, &asize, (CUdeviceptr)p) != CUDA_SUCCESS) return false;
+  const uint64_t last = (uint64_t)(base + (cols - 1) * ld + 16 * nblk);  // one past the over-read
+  if ((uint64_t)base < abase || last > abase + asize) return false;
+  if (nblk > (1l << 31) || ld * 8 >= (1l << 40)) return false;
+  cuuint64_t dims[3] = {16, (cuuint64_t)cols, (cuuint64_t)nblk};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 8), 128};
+  cuuint32_t box[3] = {16, 16, (cuuint32_t)(gemm::BM / 16)};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)base, dims, strides, box,
+                        es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
 }
 
 size_t dgemm_ws_doubles(int M, int N, int K) {
@@ -451,6 +491,15 @@ int dgemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, 
   if (tb) UTV_CHECK(make_map(&mB, Buse, N, K, ldbuse, 16, 16, &shB));
   else UTV_CHECK(make_map(&mB, Buse, K, N, ldbuse, 16, gemm::BN, &shB));
   const int a_sh = ta ? 0 : shA, b_sh = tb ? shB : 0;
+  int a3d = 0, b3d = 0;
+  if (!ta) {
+    CUtensorMap m3;
+    if (make_map3d(&m3, Ause, M, K, ldause, shA)) { mA = m3; a3d = 1; }
+  }
+  if (tb) {
+    CUtensorMap m3;
+    if (make_map3d(&m3, Buse, N, K, ldbuse, shB)) { mB = m3; b3d = 1; }
+  }
   const int k_sh = ta ? shA : (!tb ? shB : 0);
 
   const int tm = ceil_div(M + a_sh, gemm::BM), tn = ceil_div(N + b_sh, gemm::BN);
@@ -484,6 +533,7 @@ int dgemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, 
   gemm::Args a;
   a.M = M; a.N = N; a.K = K;
   a.a_sh = a_sh; a.b_sh = b_sh; a.k_sh = k_sh; a.c_sh = c_sh;
+  a.a3d = a3d; a.b3d = b3d;
   a.k_split = kper;
   a.tm = tm; a.tn = tn; a.tiles = tm * tn * splits;
   a.alpha = alpha; a.beta = beta;
