@@ -129,11 +129,12 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
                : "d"(a), "d"(b));
 }
 
-// Grid-wide barrier for cooperative launches: monotone counter, one arrival per CTA.
+// Grid-wide barrier for cooperative launches: monotone counter, one arrival per
+// CTA.  bar.sync orders the CTA's writes before thread 0's gpu-scope release
+// (cumulative), the acquire load + bar.sync publish everyone else's writes.
 __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
     unsigned int v;
     do {

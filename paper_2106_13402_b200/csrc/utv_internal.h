@@ -57,6 +57,11 @@ int set_diag(double* A, long lda, int nr, int nc, const double* d, cudaStream_t 
 // and the forward compact-WY triangle Tw (cols x cols) are written out.
 // thr_src: device scalar holding ||input||_F^2 (threshold = eps*sqrt(.)).
 size_t geqrf_ws_doubles(int rows, int cols, bool want_t);
+// Fused single-launch panel QR (panel.cu), cols <= QR_PANEL, rows <= panel_rows_max():
+// P <- R, Y, T (full cols x cols forward triangle; T must be zero below the diagonal).
+size_t panel_ws_doubles();
+int panel_rows_max();
+int panel_qr(Mat P, Mat Y, Mat T, const double* fro2, double* ws, cudaStream_t st);
 int geqrf(Mat P, Mat Y, Mat Tw, bool want_t, double* ws, size_t ws_doubles, cudaStream_t st);
 
 // ---- K2 compact-WY apply (qr.cu) ----
