@@ -67,6 +67,37 @@ int utv_dlarfb(char side, char trans, int m, int n, int k, int w, const double* 
                const double* T, long ldt, double* B, long ldb, void* work, size_t lwork,
                void* stream);
 
+/* Largest row count utv_dgeqrf accepts (148 CTAs x 512-row slabs); taller
+ * inputs are split into row chunks by the caller (TSQR). */
+int utv_dgeqrf_rows_max(void);
+
+/* Block utilities for the TSQR tree (LAPACK dlacpy / dlaset semantics):
+ * B <- A;  A <- alpha off the diagonal of the uplo ('U', 'L', 'A') part, beta
+ * on the diagonal;  A <- alpha diag(d) A (side 'L') or alpha A diag(d) ('R'). */
+int utv_dlacpy(int m, int n, const double* A, long lda, double* B, long ldb, void* stream);
+int utv_dlaset(char uplo, int m, int n, double alpha, double beta, double* A, long lda,
+               void* stream);
+int utv_ddiag_scale(char side, int m, int n, const double* d, double alpha, double* A, long lda,
+                    void* stream);
+/* Zero the strictly upper ('U') or strictly lower ('L') part of A (diagonal kept). */
+int utv_dtri_zero(char uplo, int m, int n, double* A, long lda, void* stream);
+
+/* Householder reconstruction for TSQR (row-sharded powerURV):
+ * in-place LU without pivoting of (A - diag(s)), m >= n, with
+ * s_j = -sign(pivot_j) (sign(0) = +1) chosen on the fly; L (unit lower) below
+ * the diagonal, U' on and above it, s (device, n) out.  For an orthonormal Q
+ * this gives hqr_full's Y = L and Twy = -U' S L1^{-T} (qr.py:71-100; LAPACK
+ * dorhr_col). */
+size_t utv_dgetrf_signed_bufsize(int m, int n);
+int utv_dgetrf_signed(int m, int n, double* A, long lda, double* s, void* work, size_t lwork,
+                      void* stream);
+
+/* B (m x n) <- B * op(A)^{-1} with op(A) upper triangular n x n:
+ * (uplo 'U', trans 'N') or (uplo 'L', trans 'T'); diag 'U' = unit. */
+size_t utv_dtrsm_bufsize(int m, int n);
+int utv_dtrsm_right(char uplo, char trans, char diag, int m, int n, const double* A, long lda,
+                    double* B, long ldb, void* work, size_t lwork, void* stream);
+
 /* Q[:, :ncols] = I - Y (T Y[:ncols, :]^T), Y is m x w.
  * Replaces materialize_q (qr.py:124-131) / hqr_thin's Q (qr.py:134-138). */
 size_t utv_dorgqr_bufsize(int m, int ncols, int w);

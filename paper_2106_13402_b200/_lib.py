@@ -50,6 +50,18 @@ SIGNATURES = {
     "utv_powerurv_f64": (c_int, [c_int, c_int, c_int, c_void_p, c_long, c_void_p, c_long,
                                  c_void_p, c_long, c_void_p, c_long, c_void_p, c_long, c_void_p,
                                  c_long, c_void_p, c_long, c_void_p, c_size_t, c_void_p]),
+    "utv_dgeqrf_rows_max": (c_int, []),
+    "utv_dlacpy": (c_int, [c_int, c_int, c_void_p, c_long, c_void_p, c_long, c_void_p]),
+    "utv_dlaset": (c_int, [c_char, c_int, c_int, c_double, c_double, c_void_p, c_long, c_void_p]),
+    "utv_dtri_zero": (c_int, [c_char, c_int, c_int, c_void_p, c_long, c_void_p]),
+    "utv_ddiag_scale": (c_int, [c_char, c_int, c_int, c_void_p, c_double, c_void_p, c_long,
+                                c_void_p]),
+    "utv_dgetrf_signed_bufsize": (c_size_t, [c_int, c_int]),
+    "utv_dgetrf_signed": (c_int, [c_int, c_int, c_void_p, c_long, c_void_p, c_void_p, c_size_t,
+                                  c_void_p]),
+    "utv_dtrsm_bufsize": (c_size_t, [c_int, c_int]),
+    "utv_dtrsm_right": (c_int, [c_char, c_char, c_char, c_int, c_int, c_void_p, c_long, c_void_p,
+                                c_long, c_void_p, c_size_t, c_void_p]),
     "utv_launch_count": (ctypes.c_longlong, []),
     "utv_profile_begin": (None, []),
     "utv_profile_end": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
@@ -102,21 +114,34 @@ def even_ld(rows):
 
 @dataclass
 class DMat:
-    """Column-major FP64 device matrix backed by a torch tensor of shape (cols, ld)."""
+    """Column-major FP64 device matrix: a view into a torch tensor of shape
+    (cols_total, ld) starting at element offset `off`."""
     t: object
     rows: int
     cols: int
     ld: int
+    off: int = 0
 
     @property
     def ptr(self):
-        return self.t.data_ptr()
+        return self.t.data_ptr() + 8 * self.off
 
     def at(self, r, c):
-        return self.t.data_ptr() + 8 * (r + c * self.ld)
+        return self.ptr + 8 * (r + c * self.ld)
+
+    def sub(self, r0, c0, nr, nc):
+        """View of rows r0:r0+nr, columns c0:c0+nc (no copy)."""
+        if r0 < 0 or c0 < 0 or r0 + nr > self.rows or c0 + nc > self.cols:
+            raise IndexError("DMat.sub out of range")
+        return DMat(self.t, nr, nc, self.ld, self.off + r0 + c0 * self.ld)
+
+    def tensor(self):
+        """(cols, rows) strided torch view of the block (column j = row j of the view)."""
+        return self.t.as_strided((self.cols, self.rows), (self.ld, 1),
+                                 self.t.storage_offset() + self.off)
 
     def to_numpy(self):
-        host = self.t[:, :self.rows].cpu().numpy()      # (cols, rows) C order
+        host = self.tensor().cpu().numpy()              # (cols, rows) C order
         return host.T                                   # (rows, cols) F order
 
 

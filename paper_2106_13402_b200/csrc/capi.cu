@@ -88,8 +88,88 @@ int utv_dlarfb(char side, char trans, int m, int n, int k, int w, const double* 
   if (!ld_ok(ldy, k)) return -8;
   if (!ld_ok(ldt, w)) return -10;
   if (!ld_ok(ldb, m)) return -12;
+  // wide factors: apply panel by panel (only the QR_PANEL diagonal blocks of
+  // T are read; identical result, no w x w x rows middle product)
+  if (w > QR_PANEL)
+    return larfb_panels(left ? 'L' : 'R', tr, Mat{(double*)Y, ldy, k, w}, Mat{(double*)T, ldt, w, w},
+                        Mat{Bm, ldb, m, n}, (double*)work, lwork / sizeof(double), S(stream));
   return larfb(left ? 'L' : 'R', tr, Mat{(double*)Y, ldy, k, w}, Mat{(double*)T, ldt, w, w},
                Mat{Bm, ldb, m, n}, (double*)work, lwork / sizeof(double), S(stream));
+}
+
+int utv_dgeqrf_rows_max(void) { return panel_rows_max(); }
+
+int utv_dlacpy(int m, int n, const double* A, long lda, double* Bm, long ldb, void* stream) {
+  if (m < 0) return -1;
+  if (n < 0) return -2;
+  if (lda < m) return -4;
+  if (ldb < m) return -6;
+  return copy_mat(A, lda, Bm, ldb, m, n, S(stream));
+}
+
+int utv_dlaset(char uplo, int m, int n, double alpha, double beta, double* A, long lda,
+               void* stream) {
+  int u;
+  if (uplo == 'U' || uplo == 'u') u = 1;
+  else if (uplo == 'L' || uplo == 'l') u = 2;
+  else if (uplo == 'A' || uplo == 'a') u = 0;
+  else return -1;
+  if (m < 0) return -2;
+  if (n < 0) return -3;
+  if (lda < m) return -7;
+  return laset(u, m, n, alpha, beta, A, lda, S(stream));
+}
+
+int utv_dtri_zero(char uplo, int m, int n, double* A, long lda, void* stream) {
+  int u;
+  if (uplo == 'U' || uplo == 'u') u = 3;
+  else if (uplo == 'L' || uplo == 'l') u = 4;
+  else return -1;
+  if (m < 0) return -2;
+  if (n < 0) return -3;
+  if (lda < m) return -5;
+  return laset(u, m, n, 0.0, 0.0, A, lda, S(stream));
+}
+
+int utv_ddiag_scale(char side, int m, int n, const double* d, double alpha, double* A, long lda,
+                    void* stream) {
+  const bool left = (side == 'L' || side == 'l');
+  if (!left && side != 'R' && side != 'r') return -1;
+  if (m < 0) return -2;
+  if (n < 0) return -3;
+  if (lda < m) return -7;
+  return diag_scale(left ? 0 : 1, m, n, d, alpha, A, lda, S(stream));
+}
+
+size_t utv_dgetrf_signed_bufsize(int, int) { return B(lu_ws_doubles()); }
+
+int utv_dgetrf_signed(int m, int n, double* A, long lda, double* s, void* work, size_t lwork,
+                      void* stream) {
+  if (m < 1) return -1;
+  if (n < 1 || n > m) return -2;
+  if (!ld_ok(lda, m)) return -4;
+  if (lwork < lu_ws_doubles() * sizeof(double)) return UTV_ERR_WORKSPACE;
+  return getrf_signed(Mat{A, lda, m, n}, s, (double*)work, lwork / sizeof(double), S(stream));
+}
+
+size_t utv_dtrsm_bufsize(int, int) { return B(lu_ws_doubles()); }
+
+int utv_dtrsm_right(char uplo, char trans, char diag, int m, int n, const double* A, long lda,
+                    double* Bm, long ldb, void* work, size_t lwork, void* stream) {
+  const bool up = (uplo == 'U' || uplo == 'u');
+  if (!up && uplo != 'L' && uplo != 'l') return -1;
+  const bool tr = (trans == 'T' || trans == 't');
+  if (!tr && trans != 'N' && trans != 'n') return -2;
+  const bool unit = (diag == 'U' || diag == 'u');
+  if (!unit && diag != 'N' && diag != 'n') return -3;
+  if (up == tr) return -2;  // only op(A) upper: (U, N) or (L, T)
+  if (m < 0) return -4;
+  if (n < 0) return -5;
+  if (!ld_ok(lda, n)) return -7;
+  if (!ld_ok(ldb, m)) return -9;
+  if (lwork < lu_ws_doubles() * sizeof(double)) return UTV_ERR_WORKSPACE;
+  return trsm_right_upper(tr, unit, n, A, lda, Mat{Bm, ldb, m, n}, (double*)work,
+                          lwork / sizeof(double), S(stream));
 }
 
 size_t utv_dorgqr_bufsize(int m, int ncols, int w) {

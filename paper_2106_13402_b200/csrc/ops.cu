@@ -88,6 +88,32 @@ __global__ void copy_kernel(const double* __restrict__ S, long lds, double* __re
   }
 }
 
+// LAPACK dlaset semantics: uplo 0 = whole, 1 = strictly upper + diag,
+// 2 = strictly lower + diag; off-diagonal entries <- alpha, diagonal <- beta.
+// uplo 3 / 4: strictly upper / lower part only (diagonal untouched).
+__global__ void laset_kernel(double* A, long lda, int rows, int cols, int uplo, double alpha,
+                             double beta) {
+  const long total = (long)rows * cols;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total;
+       i += (long)gridDim.x * blockDim.x) {
+    const int r = (int)(i % rows), c = (int)(i / rows);
+    if (r == c) { if (uplo < 3) A[r + (long)c * lda] = beta; }
+    else if (uplo == 3 ? r < c : (uplo == 4 ? r > c : false)) A[r + (long)c * lda] = alpha;
+    else if (uplo == 0 || (uplo == 1 && r < c) || (uplo == 2 && r > c)) A[r + (long)c * lda] = alpha;
+  }
+}
+
+// A <- alpha * diag(d) A (rows, side 0) or alpha * A diag(d) (cols, side 1).
+__global__ void dscale_kernel(double* A, long lda, int rows, int cols, const double* d, int side,
+                              double alpha) {
+  const long total = (long)rows * cols;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total;
+       i += (long)gridDim.x * blockDim.x) {
+    const int r = (int)(i % rows), c = (int)(i / rows);
+    A[r + (long)c * lda] *= alpha * d[side == 0 ? r : c];
+  }
+}
+
 inline int grid_for(long total) {
   const long g = (total + 255) / 256;
   const long cap = 8L * num_sms();
@@ -134,6 +160,26 @@ int copy_mat(const double* src, long lds, double* dst, long ldd, int rows, int c
   if (rows <= 0 || cols <= 0) return UTV_OK;
   UTV_CUDA(cudaMemcpy2DAsync(dst, ldd * sizeof(double), src, lds * sizeof(double),
                              rows * sizeof(double), cols, cudaMemcpyDeviceToDevice, st));
+  return UTV_OK;
+}
+
+int laset(int uplo, int rows, int cols, double alpha, double beta, double* A, long lda,
+          cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return UTV_OK;
+  ProfScope ps(PROF_OPS, 0.0, 8.0 * rows * cols, st);
+  ops::laset_kernel<<<ops::grid_for((long)rows * cols), 256, 0, st>>>(A, lda, rows, cols, uplo,
+                                                                      alpha, beta);
+  UTV_CUDA(cudaGetLastError());
+  return UTV_OK;
+}
+
+int diag_scale(int side, int rows, int cols, const double* d, double alpha, double* A, long lda,
+               cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return UTV_OK;
+  ProfScope ps(PROF_OPS, (double)rows * cols, 16.0 * rows * cols, st);
+  ops::dscale_kernel<<<ops::grid_for((long)rows * cols), 256, 0, st>>>(A, lda, rows, cols, d, side,
+                                                                       alpha);
+  UTV_CUDA(cudaGetLastError());
   return UTV_OK;
 }
 

@@ -91,6 +91,39 @@ __global__ void __launch_bounds__(THREADS, 1) panel_qr_kernel(Args a) {
     if (G > 1) grid_barrier(a.ctr, nbar * (unsigned)G);
     else __syncthreads();
   };
+  // Split barrier: arrive, do independent work, then wait.
+  auto garrive = [&]() {
+    ++nbar;
+    __syncthreads();
+    if (G > 1 && t == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.ctr) : "memory");
+  };
+  auto gwait = [&]() {
+    if (G > 1 && t == 0) {
+      unsigned v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.ctr) : "memory");
+      } while (v < nbar * (unsigned)G);
+    }
+    __syncthreads();
+  };
+  // Leaf-triangle column pj (qr.py:63-68), computed redundantly in every CTA
+  // while the next column's grid barrier is in flight:
+  // Ts[r][pj] = -tau * sum_{q=r}^{pj-1} Ts[r][q] Z[q], 4 rows per warp.
+  int pend = -1;
+  double ptau = 0.0;
+  auto ts_column = [&]() {
+    if (pend < 0) return;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int r = warp * 4 + k;
+      double s = (lane >= r && lane < pend) ? Ts[r + lane * (NB + 1)] * Zv[lane] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0 && r < pend) Ts[r + pend * (NB + 1)] = -ptau * s;
+    }
+    if (t == 0) Ts[pend + pend * (NB + 1)] = ptau;
+    pend = -1;
+  };
 
   for (int l = 0; l < nleaf; ++l) {
     const int j0 = l * NB;
@@ -129,7 +162,9 @@ __global__ void __launch_bounds__(THREADS, 1) panel_qr_kernel(Args a) {
         }
         a.part[((size_t)par * G + g) * 2 * NB + t] = s;
       }
-      gsync();
+      garrive();
+      ts_column();  // previous column's triangle entries, hidden behind the barrier
+      gwait();
       {  // every CTA: sum the G records, 4 interleaved groups, all loads in flight, fixed order
         const int e = t & 63, q0 = t >> 6;
         double v[PMAX];
@@ -176,17 +211,8 @@ __global__ void __launch_bounds__(THREADS, 1) panel_qr_kernel(Args a) {
           }
         }
         if (owner && t < NB && t > jj && t < jb) tile[(J - r0) + t * ld] -= Wv[t];
-        // leaf triangle column jj (qr.py:63-68), redundantly in every CTA:
-        // Ts[r][jj] = -tau * sum_{q=r}^{jj-1} Ts[r][q] Z[q], 4 rows per warp
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int r = warp * 4 + k;
-          double s = (lane >= r && lane < jj) ? Ts[r + lane * (NB + 1)] * Zv[lane] : 0.0;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-          if (lane == 0 && r < jj) Ts[r + jj * (NB + 1)] = -tau * s;
-        }
-        if (t == 0) Ts[jj + jj * (NB + 1)] = tau;
+        pend = jj;
+        ptau = tau;
         __syncthreads();
         for (int i = i_lo + t; i < nr; i += THREADS) tile[i + jj * ld] = vrow[i];
         if (owner && t == 0) tile[(J - r0) + jj * ld] = -sgn * xnorm;
@@ -195,6 +221,8 @@ __global__ void __launch_bounds__(THREADS, 1) panel_qr_kernel(Args a) {
       }
       __syncthreads();
     }
+    ts_column();  // last column of the leaf
+    __syncthreads();
 
     // ---- write R / Y of the leaf; turn the tile into Y form ----
     for (int idx = t; idx < nr * jb; idx += THREADS) {

@@ -48,6 +48,12 @@ int set_identity(double* A, long lda, int rows, int cols, cudaStream_t st);
 int set_zero(double* A, long lda, int rows, int cols, cudaStream_t st);
 int copy_mat(const double* src, long lds, double* dst, long ldd, int rows, int cols,
              cudaStream_t st);
+// LAPACK dlaset: uplo 0 all / 1 upper / 2 lower off-diagonal <- alpha, diagonal <- beta.
+int laset(int uplo, int rows, int cols, double alpha, double beta, double* A, long lda,
+          cudaStream_t st);
+// A <- alpha diag(d) A (side 0) or alpha A diag(d) (side 1).
+int diag_scale(int side, int rows, int cols, const double* d, double alpha, double* A, long lda,
+               cudaStream_t st);
 // diag block: A[:nr, :nc] = 0 except A[i,i] = d[i] (i < min(nr, nc)).
 int set_diag(double* A, long lda, int nr, int nc, const double* d, cudaStream_t st);
 
@@ -85,6 +91,14 @@ int orgqr_panels(Mat Y, Mat T, Mat Q, double* ws, size_t ws_doubles, cudaStream_
 // forward compact-WY triangle of the whole product (qr.py:63-68 semantics).
 size_t build_t_ws_doubles(int rows, int cols);
 int build_t(Mat Y, Mat T, double* ws, size_t ws_doubles, cudaStream_t st);
+
+// ---- Householder reconstruction for TSQR (lu.cu) ----
+// In-place LU without pivoting of (P - diag(s)), rows >= cols, s_j = -sign(pivot_j).
+int getrf_signed(Mat P, double* s, double* ws, size_t ws_doubles, cudaStream_t st);
+// B <- B * op(A)^{-1}, op(A) upper triangular (A upper + !trans, or A lower + trans).
+int trsm_right_upper(bool trans, bool unit, int n, const double* A, long lda, Mat B, double* ws,
+                     size_t ws_doubles, cudaStream_t st);
+size_t lu_ws_doubles();
 
 // ---- K6 Jacobi SVD (jacobi.cu) ----
 // A (n x n, read only): sigma (desc, device), U (n x n), V (n x n) with the

@@ -149,3 +149,62 @@ class PowerUrvRun:
             self.m, self.n, self.q, A.ptr, A.ld, G.ptr, G.ld, self.Uy.ptr, self.Uy.ld, self.Ut.ptr,
             self.Ut.ld, self.R.ptr, self.R.ld, self.Vy.ptr, self.Vy.ld, self.Vt.ptr, self.Vt.ld,
             self.ws.data_ptr(), self.lw, stream_ptr()), "utv_powerurv_f64")
+
+
+# ---------------------------------------------------------------------------
+# TSQR / Householder-reconstruction building blocks (row-sharded powerURV)
+# ---------------------------------------------------------------------------
+
+def geqrf_rows_max():
+    return int(load().utv_dgeqrf_rows_max())
+
+
+def lacpy(A: DMat, B: DMat):
+    check(load().utv_dlacpy(A.rows, A.cols, A.ptr, A.ld, B.ptr, B.ld, stream_ptr()), "utv_dlacpy")
+    return B
+
+
+def copy(A: DMat):
+    return lacpy(A, dempty(A.rows, A.cols))
+
+
+def laset(uplo, alpha, beta, A: DMat):
+    check(load().utv_dlaset(uplo.encode(), A.rows, A.cols, alpha, beta, A.ptr, A.ld, stream_ptr()),
+          "utv_dlaset")
+    return A
+
+
+def tri_zero(uplo, A: DMat):
+    """Zero the strictly upper ('U') or strictly lower ('L') part; diagonal kept."""
+    check(load().utv_dtri_zero(uplo.encode(), A.rows, A.cols, A.ptr, A.ld, stream_ptr()),
+          "utv_dtri_zero")
+    return A
+
+
+def diag_scale(side, d, A: DMat, alpha=1.0):
+    """A <- alpha diag(d) A (side 'L') or alpha A diag(d) (side 'R'); d a device tensor."""
+    check(load().utv_ddiag_scale(side.encode(), A.rows, A.cols, d.data_ptr(), alpha, A.ptr, A.ld,
+                                 stream_ptr()), "utv_ddiag_scale")
+    return A
+
+
+def getrf_signed(A: DMat):
+    """In place LU without pivoting of (A - diag(s)); returns s (device tensor)."""
+    import torch
+    lib = load()
+    s = torch.empty(max(A.cols, 1), dtype=torch.float64, device="cuda")
+    lw = lib.utv_dgetrf_signed_bufsize(A.rows, A.cols)
+    ws = workspace(lw)
+    check(lib.utv_dgetrf_signed(A.rows, A.cols, A.ptr, A.ld, s.data_ptr(), ws.data_ptr(), lw,
+                                stream_ptr()), "utv_dgetrf_signed")
+    return s
+
+
+def trsm_right(uplo, trans, diag, A: DMat, B: DMat):
+    """B <- B op(A)^{-1}, op(A) upper triangular."""
+    lib = load()
+    lw = lib.utv_dtrsm_bufsize(B.rows, B.cols)
+    ws = workspace(lw)
+    check(lib.utv_dtrsm_right(uplo.encode(), trans.encode(), diag.encode(), B.rows, B.cols, A.ptr,
+                              A.ld, B.ptr, B.ld, ws.data_ptr(), lw, stream_ptr()), "utv_dtrsm_right")
+    return B
