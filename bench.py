@@ -381,6 +381,83 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
+# ---------------------------------------------------------------------------
+# C4: row-sharded powerURV on a tall matrix (strong scaling over ranks)
+# ---------------------------------------------------------------------------
+
+C4_METRIC = "row-sharded powerURV q=1, 524288x4096 fp64: FP64 TFLOP/s (algorithmic, SURVEY §8d)"
+
+
+def run_c4(args):
+    import torch
+    ws, rank, local = dist_env()
+    from paper_2106_13402_b200 import sharded
+    import paper_2106_13402_b200 as pk
+    from paper_2106_13402_b200 import _lib
+    from paper_2106_13402_b200._lib import dempty
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        comm = sharded.TorchComm()
+    else:
+        comm = sharded.Comm()
+    m, n, q = args.c4_rows, args.c4_cols, 1
+    rows = [m // ws + (1 if r < m % ws else 0) for r in range(ws)]
+    gen = torch.Generator(device="cuda").manual_seed(40 + rank)
+    a = dempty(rows[rank], n)
+    a.t.normal_(generator=gen)                     # i.i.d. N(0,1) rows (PAPER.md:843 timing input)
+    g = _lib.dfrom_numpy(pk.gaussian(n, n, pk.RngStream(4)))
+    torch.cuda.synchronize()
+
+    def step():
+        return sharded.power_urv_sharded(a, g, q, comm)
+
+    def sync_all():
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+            torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        out = step()
+        del out
+    sync_all()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = _lib.launch_count()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(args.steps):
+        out = step()
+        del out
+    t1.record()
+    sync_all()
+    clk = clocks.stop()
+    launches = _lib.launch_count() - launches0
+    secs = t0.elapsed_time(t1) / 1e3
+    if ws > 1:
+        tt = torch.tensor([secs], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        secs = float(tt.item())
+    per = secs / args.steps
+    flops = powerurv_flops(m, n, q)
+    line = {"metric": C4_METRIC, "value": flops / per / 1e12, "unit": "TFLOP/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (device N(0,1) rows per rank; G from the reference PCG64 stream)",
+            "config": {"workload": f"C4 powerURV q={q} on {m}x{n} fp64, row-sharded over {ws} rank(s)",
+                       "rows_per_rank": rows, "parallelism": f"row shards x{ws} (NCCL allreduce + TSQR)",
+                       "l2_policy": "inputs (16 GiB / ranks) larger than L2"},
+            "frac_of_fp64_peak": flops / per / 1e12 / ws / FP64_PEAK_TFLOPS,
+            "gpu_launches": int(launches), "clocks": clk, "e2e": None, "cpu_baseline": None}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -392,8 +469,15 @@ def main():
     ap.add_argument("--q", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workload", choices=["headline", "c4"], default="headline",
+                    help="headline = BASELINE metric (n=16384 powerURV + randUTV); "
+                         "c4 = row-sharded tall powerURV (BASELINE configs[3])")
+    ap.add_argument("--c4-rows", type=int, default=524288)
+    ap.add_argument("--c4-cols", type=int, default=4096)
     args = ap.parse_args()
-    if args.impl == "reference":
+    if args.workload == "c4" and args.impl != "reference":
+        run_c4(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

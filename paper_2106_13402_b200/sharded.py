@@ -348,7 +348,9 @@ def power_urv_sharded(a_loc, g, q, comm=None, ops=None, chunk_rows=None):
         for it in range(q):                          # powerurv.py:63-68
             yhat = ops.gemm("N", "N", 1.0, a_loc, v)                 # :64
             vhat, _ = tsqr(yhat, comm, ops, chunk_rows)              # :65
+            del yhat
             y = ops.gemm("T", "N", 1.0, a_loc, vhat)                 # :66 (partial)
+            del vhat
             if comm.size > 1:
                 comm.sync()
                 ty = ops.to_comm(y)
@@ -360,5 +362,6 @@ def power_urv_sharded(a_loc, g, q, comm=None, ops=None, chunk_rows=None):
     ahat = ops.copy(a_loc)                                           # :70
     ops.larfb("R", False, vy, vt, ahat)
     qh, r_in = tsqr(ahat, comm, ops, chunk_rows)                     # :71
+    del ahat
     uy, ut, r, _ = householder_from_q(qh, r_in, comm, ops)
     return {"Uy": uy, "Ut": ut, "R": r, "Vy": vy, "Vt": vt}
