@@ -43,6 +43,14 @@ int utv_dgemm(char transa, char transb, int m, int n, int k, double alpha, const
               long lda, const double* B, long ldb, double beta, double* C, long ldc, void* work,
               size_t lwork, void* stream);
 
+/* FP32 C = alpha*op(A)*op(B) + beta*C on the tcgen05 tensor cores with the
+ * 3xTF32 split (hi*hi + hi*lo + lo*hi, hi = rna_tf32(x)): FP32-level accuracy
+ * for the fp32 randUTV variant (BASELINE C5).  lda/ldb multiples of 4, A/B
+ * 16-byte aligned (TMA). */
+int utv_sgemm_tf32x3(char transa, char transb, int m, int n, int k, float alpha, const float* A,
+                     long lda, const float* B, long ldb, float beta, float* C, long ldc,
+                     void* stream);
+
 /* Sum of squares of an m x n block -> *out (device scalar).
  * Replaces frobenius_norm (matrix.py:79-81) and ErrorTracker.update's panel
  * mass (randutv.py:52-62). */

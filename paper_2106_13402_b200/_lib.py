@@ -51,6 +51,8 @@ SIGNATURES = {
                                  c_void_p, c_long, c_void_p, c_long, c_void_p, c_long, c_void_p,
                                  c_long, c_void_p, c_long, c_void_p, c_size_t, c_void_p]),
     "utv_dgeqrf_rows_max": (c_int, []),
+    "utv_sgemm_tf32x3": (c_int, [c_char, c_char, c_int, c_int, c_int, ctypes.c_float, c_void_p, c_long,
+                                 c_void_p, c_long, ctypes.c_float, c_void_p, c_long, c_void_p]),
     "utv_dlacpy": (c_int, [c_int, c_int, c_void_p, c_long, c_void_p, c_long, c_void_p]),
     "utv_dlaset": (c_int, [c_char, c_int, c_int, c_double, c_double, c_void_p, c_long, c_void_p]),
     "utv_dtri_zero": (c_int, [c_char, c_int, c_int, c_void_p, c_long, c_void_p]),
@@ -67,8 +69,8 @@ SIGNATURES = {
     "utv_profile_end": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
 }
 
-PROF_CATEGORIES = ("dgemm_dmma", "splitk_reduce", "panel_qr_leaf", "jacobi_rounds",
-                   "jacobi_finish", "small_ops")
+PROF_CATEGORIES = ("dgemm_dmma", "splitk_reduce", "panel_qr", "jacobi_rounds",
+                   "jacobi_finish", "small_ops", "sgemm_tf32x3")
 
 
 def load():
@@ -123,11 +125,15 @@ class DMat:
     off: int = 0
 
     @property
+    def esize(self):
+        return self.t.element_size()
+
+    @property
     def ptr(self):
-        return self.t.data_ptr() + 8 * self.off
+        return self.t.data_ptr() + self.esize * self.off
 
     def at(self, r, c):
-        return self.ptr + 8 * (r + c * self.ld)
+        return self.ptr + self.esize * (r + c * self.ld)
 
     def sub(self, r0, c0, nr, nc):
         """View of rows r0:r0+nr, columns c0:c0+nc (no copy)."""
@@ -145,10 +151,13 @@ class DMat:
         return host.T                                   # (rows, cols) F order
 
 
-def dempty(rows, cols, ld=None):
+def dempty(rows, cols, ld=None, dtype=None):
     torch = torch_cuda()
-    ld = even_ld(rows) if ld is None else ld
-    t = torch.empty((max(cols, 1), ld), dtype=torch.float64, device="cuda")
+    dtype = torch.float64 if dtype is None else dtype
+    if ld is None:
+        # fp64: even ld (TMA 16-byte strides); fp32: multiple of 4
+        ld = even_ld(rows) if dtype == torch.float64 else max(4, (rows + 3) // 4 * 4)
+    t = torch.empty((max(cols, 1), ld), dtype=dtype, device="cuda")
     return DMat(t, rows, cols, ld)
 
 
@@ -166,12 +175,13 @@ def deye(n):
     return m
 
 
-def dfrom_numpy(a, pinned=False):
-    """Copy a 2-D float64 array to the device (column-major, even ld)."""
+def dfrom_numpy(a, pinned=False, dtype=None):
+    """Copy a 2-D array to the device (column-major; float64 unless dtype=float32)."""
     torch = torch_cuda()
-    a = np.asfortranarray(a, dtype=np.float64)
+    npdt = np.float32 if dtype == torch.float32 else np.float64
+    a = np.asfortranarray(a, dtype=npdt)
     rows, cols = a.shape
-    m = dempty(rows, cols)
+    m = dempty(rows, cols, dtype=torch.float32 if npdt == np.float32 else torch.float64)
     src = torch.from_numpy(a.T)             # (cols, rows) view of the F-order data
     if pinned:
         src = src.pin_memory()

@@ -99,6 +99,21 @@ int utv_dlarfb(char side, char trans, int m, int n, int k, int w, const double* 
 
 int utv_dgeqrf_rows_max(void) { return panel_rows_max(); }
 
+int utv_sgemm_tf32x3(char transa, char transb, int m, int n, int k, float alpha, const float* A,
+                     long lda, const float* Bm, long ldb, float beta, float* C, long ldc,
+                     void* stream) {
+  const bool ta = (transa == 'T' || transa == 't'), tb = (transb == 'T' || transb == 't');
+  if (!ta && transa != 'N' && transa != 'n') return -1;
+  if (!tb && transb != 'N' && transb != 'n') return -2;
+  if (m < 0) return -3;
+  if (n < 0) return -4;
+  if (k < 0) return -5;
+  if (k > 0 && (lda < (ta ? k : m) || (lda & 3))) return -8;
+  if (k > 0 && (ldb < (tb ? n : k) || (ldb & 3))) return -10;
+  if (ldc < (m > 1 ? m : 1)) return -13;
+  return sgemm_tf32x3(ta, tb, m, n, k, alpha, A, lda, Bm, ldb, beta, C, ldc, S(stream));
+}
+
 int utv_dlacpy(int m, int n, const double* A, long lda, double* Bm, long ldb, void* stream) {
   if (m < 0) return -1;
   if (n < 0) return -2;

@@ -1,0 +1,399 @@
+// K10: FP32 GEMM on the 5th-generation tensor cores, 3xTF32 split.
+//
+//   C = alpha * op(A) * op(B) + beta * C      (fp32, column-major, op in {N, T})
+//
+// The fp32 variant of randUTV (BASELINE C5) needs
+// FP32-accurate products: plain TF32 sampling wrecks rank revelation
+// (SURVEY §7 hard part 6).  Every operand element is split x = hi + lo with
+// hi = rna_tf32(x) and lo = x - hi (exact in fp32); the tensor cores
+// accumulate hi*hi + hi*lo + lo*hi in FP32 (TMEM).  With hi rounded to
+// nearest, |lo| <= 2^-11 |x| and the (truncated) tf32 lo loses at most
+// 2^-22 |x|: the product error is fp32-level.
+//
+// Design (sm_100a, warp-specialised, persistent):
+//   warp 0      TMA producer: raw fp32 tiles A (128 x 32) and B (128 x 32)
+//               into a RAW_STAGES ring (mbarrier full/empty, expect_tx)
+//   warp 1      TMEM allocator + MMA issuer (one elected lane):
+//               12 x tcgen05.mma.cta_group::1.kind::tf32 (M=128, N=128, K=8)
+//               per 32-deep k-block, tcgen05.commit -> mbarriers
+//   warps 4-11  converters: raw tile (K- or MN-major) -> hi / lo tiles in
+//               the canonical K-major 128B-swizzled UMMA layout (also turns
+//               MN-major operands K-major, so one descriptor form serves all
+//               four op combinations); fence.proxy.async before arrival
+//   warps 12-15 epilogue: tcgen05.ld 32x32b from a double-buffered TMEM
+//               accumulator (2 x 128 columns), alpha/beta, coalesced stores;
+//               overlaps the next tile's MMAs.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "utv_internal.h"
+
+namespace utv {
+
+namespace tf32 {
+constexpr int BM = 128, BN = 128, BK = 32;
+constexpr int RAW_STAGES = 2, CONV_STAGES = 2, ACC_STAGES = 2;
+constexpr int THREADS = 512;                  // 16 warps
+constexpr int CONV_WARP0 = 4, NCONV = 8;      // converter warps 4..11
+constexpr int EPI_WARP0 = 12;                 // epilogue warps 12..15
+constexpr uint32_t TILE_BYTES = BM * BK * 4;  // 16 KB (A or B, raw or hi or lo)
+constexpr uint32_t RAW_BYTES = 2 * TILE_BYTES;
+constexpr uint32_t CONV_BYTES = 4 * TILE_BYTES;  // hiA loA hiB loB
+constexpr size_t SMEM = (size_t)RAW_STAGES * RAW_BYTES + (size_t)CONV_STAGES * CONV_BYTES + 1024 + 256;
+constexpr uint32_t TMEM_COLS = ACC_STAGES * BN;  // 256
+
+struct Args {
+  int M, N, K;
+  int tm, tn, tiles;
+  float alpha, beta;
+  float* C;
+  long ldc;
+};
+
+// K-major, 128B-swizzled UMMA shared-memory descriptor (SM100, version 1):
+// rows of 128 B, 8-row atoms 1024 B apart (SBO), LBO unused (1).
+__device__ __forceinline__ uint64_t kmajor_sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                 // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;       // SBO
+  d |= (uint64_t)1 << 46;                 // version (Blackwell)
+  d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
+  return d;
+}
+
+// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, M=128, N=128.
+__host__ __device__ constexpr uint32_t idesc_tf32() {
+  return (1u << 4)                    // c_format F32
+         | (2u << 7)                  // a_format TF32
+         | (2u << 10)                 // b_format TF32
+         | ((uint32_t)(BN >> 3) << 17)
+         | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc_tf32()), "r"(accum));
+}
+
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_after_sync() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_before_sync() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float rna_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(THREADS, 1)
+    sgemm_tf32x3_kernel(const __grid_constant__ CUtensorMap tmA,
+                        const __grid_constant__ CUtensorMap tmB, const Args p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char* raw = smem;                                   // [RAW_STAGES][A | B]
+  unsigned char* conv = raw + RAW_STAGES * RAW_BYTES;          // [CONV_STAGES][hiA loA hiB loB]
+  uint64_t* bars = (uint64_t*)(conv + CONV_STAGES * CONV_BYTES);
+  const uint32_t raw_full = smem_u32(bars), raw_empty = raw_full + 8 * RAW_STAGES;
+  const uint32_t conv_full = raw_empty + 8 * RAW_STAGES, conv_empty = conv_full + 8 * CONV_STAGES;
+  const uint32_t acc_full = conv_empty + 8 * CONV_STAGES, acc_empty = acc_full + 8 * ACC_STAGES;
+  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * (RAW_STAGES + CONV_STAGES + ACC_STAGES));
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nk = (p.K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < RAW_STAGES; ++s) {
+      mbar_init(raw_full + 8 * s, 1);
+      mbar_init(raw_empty + 8 * s, NCONV);
+    }
+    for (int s = 0; s < CONV_STAGES; ++s) {
+      mbar_init(conv_full + 8 * s, NCONV);
+      mbar_init(conv_empty + 8 * s, 1);
+    }
+    for (int s = 0; s < ACC_STAGES; ++s) {
+      mbar_init(acc_full + 8 * s, 1);
+      mbar_init(acc_empty + 8 * s, 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ================= TMA producer =================
+    if (lane == 0) {
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmB);
+      long g = 0;
+      for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+        const int mc = (tile % p.tm) * BM, nc = (tile / p.tm) * BN;
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int s = (int)(g % RAW_STAGES);
+          if (g >= RAW_STAGES) mbar_wait(raw_empty + 8 * s, (uint32_t)(((g / RAW_STAGES) & 1) ^ 1));
+          const uint32_t fb = raw_full + 8 * s;
+          mbar_arrive_expect_tx(fb, RAW_BYTES);
+          const uint32_t dA = smem_u32(raw + s * RAW_BYTES), dB = dA + TILE_BYTES;
+          const int k = kb * BK;
+          // A: TA -> K-major box {32 k, 128 m}; else MN-major box {128 m, 32 k}
+          if (TA) tma_load_2d(dA, &tmA, fb, k, mc);
+          else tma_load_2d(dA, &tmA, fb, mc, k);
+          // B: !TB -> K-major box {32 k, 128 n}; else MN-major box {128 n, 32 k}
+          if (!TB) tma_load_2d(dB, &tmB, fb, k, nc);
+          else tma_load_2d(dB, &tmB, fb, nc, k);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer =================
+    long g = 0;
+    int local = 0;
+    for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x, ++local) {
+      const int as = local % ACC_STAGES;
+      if (local >= ACC_STAGES) mbar_wait(acc_empty + 8 * as, (uint32_t)(((local / ACC_STAGES) & 1) ^ 1));
+      fence_after_sync();
+      const uint32_t tmem_d = tmem_base + as * BN;
+      for (int kb = 0; kb < nk; ++kb, ++g) {
+        const int c = (int)(g % CONV_STAGES);
+        mbar_wait(conv_full + 8 * c, (uint32_t)((g / CONV_STAGES) & 1));
+        fence_after_sync();
+        if (lane == 0) {
+          const uint32_t base = smem_u32(conv + c * CONV_BYTES);
+          const uint32_t hiA = base, loA = base + TILE_BYTES, hiB = base + 2 * TILE_BYTES,
+                         loB = base + 3 * TILE_BYTES;
+#pragma unroll
+          for (int ks = 0; ks < BK / 8; ++ks) {
+            const uint32_t off = ks * 32;  // 8 tf32 = 32 bytes along K
+            const uint32_t acc0 = (kb > 0 || ks > 0) ? 1u : 0u;
+            umma_tf32(tmem_d, kmajor_sw128_desc(loA + off), kmajor_sw128_desc(hiB + off), acc0);
+            umma_tf32(tmem_d, kmajor_sw128_desc(hiA + off), kmajor_sw128_desc(loB + off), 1u);
+            umma_tf32(tmem_d, kmajor_sw128_desc(hiA + off), kmajor_sw128_desc(hiB + off), 1u);
+          }
+          umma_commit(conv_empty + 8 * c);
+          if (kb == nk - 1) umma_commit(acc_full + 8 * as);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp >= CONV_WARP0 && warp < CONV_WARP0 + NCONV) {
+    // ================= converters: raw -> hi/lo, K-major SW128 =================
+    const int ct = threadIdx.x - CONV_WARP0 * 32;  // 0..255
+    long g = 0;
+    for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+      for (int kb = 0; kb < nk; ++kb, ++g) {
+        const int s = (int)(g % RAW_STAGES), c = (int)(g % CONV_STAGES);
+        mbar_wait(raw_full + 8 * s, (uint32_t)((g / RAW_STAGES) & 1));
+        if (g >= CONV_STAGES) mbar_wait(conv_empty + 8 * c, (uint32_t)(((g / CONV_STAGES) & 1) ^ 1));
+        const float* rA = (const float*)(raw + s * RAW_BYTES);
+        const float* rB = rA + BM * BK;
+        float* cb = (float*)(conv + c * CONV_BYTES);
+        // 2 operands x 128 rows x 8 quads = 2048 quads, 8 per thread
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int idx = it * 256 + ct;
+          const int opnd = idx >> 10;          // 0 = A, 1 = B
+          const bool kmaj = opnd == 0 ? TA : !TB;
+          // K-major raw rows are 128 B: 8 consecutive threads read one row
+          // (conflict-free float4); MN-major raw: consecutive threads take
+          // consecutive rows (conflict-free scalar columns)
+          const int r = kmaj ? ((idx >> 3) & 127) : (idx & 127);  // row (m or n)
+          const int qd = kmaj ? (idx & 7) : ((idx >> 7) & 7);       // k quad
+          const float* src = opnd == 0 ? rA : rB;
+          float4 x;
+          if (kmaj) {
+            x = *(const float4*)(src + r * BK + qd * 4);
+          } else {
+            x.x = src[(qd * 4 + 0) * BM + r];
+            x.y = src[(qd * 4 + 1) * BM + r];
+            x.z = src[(qd * 4 + 2) * BM + r];
+            x.w = src[(qd * 4 + 3) * BM + r];
+          }
+          float4 h, l;
+          h.x = rna_tf32(x.x); l.x = x.x - h.x;
+          h.y = rna_tf32(x.y); l.y = x.y - h.y;
+          h.z = rna_tf32(x.z); l.z = x.z - h.z;
+          h.w = rna_tf32(x.w); l.w = x.w - h.w;
+          const int off = r * 32 + ((qd ^ (r & 7)) << 2);  // floats, 128B-swizzled
+          float* hi = cb + opnd * 2 * BM * BK;
+          float* lo = hi + BM * BK;
+          *(float4*)(hi + off) = h;
+          *(float4*)(lo + off) = l;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(conv_full + 8 * c);
+          mbar_arrive(raw_empty + 8 * s);
+        }
+      }
+    }
+  } else if (warp >= EPI_WARP0) {
+    // ================= epilogue =================
+    const int q = warp & 3;  // TMEM lane quarter
+    int local = 0;
+    for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x, ++local) {
+      const int as = local % ACC_STAGES;
+      const int mc = (tile % p.tm) * BM, nc = (tile / p.tm) * BN;
+      mbar_wait(acc_full + 8 * as, (uint32_t)((local / ACC_STAGES) & 1));
+      fence_after_sync();
+      const int m = mc + q * 32 + lane;
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        float v[16];
+        tmem_ld16(taddr + c0, v);
+        if (m < p.M) {
+          float cv[16];
+          if (p.beta != 0.0f) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int n = nc + c0 + j;
+              cv[j] = (n < p.N) ? p.C[m + (long)n * p.ldc] : 0.0f;
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int n = nc + c0 + j;
+            if (n < p.N) {
+              const float r = p.alpha * v[j];
+              p.C[m + (long)n * p.ldc] = (p.beta == 0.0f) ? r : fmaf(p.beta, cv[j], r);
+            }
+          }
+        }
+      }
+      fence_before_sync();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty + 8 * as);
+    }
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after_sync();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "n"(TMEM_COLS)
+                 : "memory");
+  }
+}
+}  // namespace tf32
+
+static PFN_cuTensorMapEncodeTiled_v12000 g_enc32 = nullptr;
+static std::once_flag g_enc32_once;
+
+static int get_enc32() {
+  std::call_once(g_enc32_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_enc32 = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    for (auto f : {tf32::sgemm_tf32x3_kernel<false, false>, tf32::sgemm_tf32x3_kernel<false, true>,
+                   tf32::sgemm_tf32x3_kernel<true, false>, tf32::sgemm_tf32x3_kernel<true, true>})
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tf32::SMEM);
+  });
+  return g_enc32 ? UTV_OK : UTV_ERR_CUDA;
+}
+
+// Plain (non-swizzled) fp32 map over a column-major rows x cols matrix.
+static int make_map32(CUtensorMap* map, const float* p, long rows, long cols, long ld, uint32_t box0,
+                      uint32_t box1) {
+  if ((ld & 3) || ((uintptr_t)p & 15)) return UTV_ERR_ALIGN;
+  cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)cols};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {box0, box1};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = g_enc32(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)p, dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    fprintf(stderr, "libutvb200: fp32 tensor map failed (%d) rows=%ld cols=%ld ld=%ld\n", (int)r,
+            rows, cols, ld);
+    return UTV_ERR_CUDA;
+  }
+  return UTV_OK;
+}
+
+__global__ void sscale_kernel(int M, int N, float beta, float* C, long ldc) {
+  const size_t total = (size_t)M * N;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int m = (int)(i % M), n = (int)(i / M);
+    float* c = C + m + (long)n * ldc;
+    *c = (beta == 0.0f) ? 0.0f : beta * *c;
+  }
+}
+
+int sgemm_tf32x3(bool ta, bool tb, int M, int N, int K, float alpha, const float* A, long lda,
+                 const float* B, long ldb, float beta, float* C, long ldc, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return UTV_OK;
+  UTV_CHECK(get_enc32());
+  if (K <= 0 || alpha == 0.0f) {
+    if (beta == 1.0f) return UTV_OK;
+    ProfScope ps(PROF_OPS, 0.0, 8.0 * M * N, st);
+    sscale_kernel<<<4 * num_sms(), 256, 0, st>>>(M, N, beta, C, ldc);
+    UTV_CUDA(cudaGetLastError());
+    return UTV_OK;
+  }
+  if (((uintptr_t)C & 3) || ldc < M) return UTV_ERR_ALIGN;
+  CUtensorMap mA, mB;
+  // A (op(A) is M x K): TA -> stored K x M (K contiguous); else M x K (M contiguous)
+  if (ta) UTV_CHECK(make_map32(&mA, A, K, M, lda, tf32::BK, tf32::BM));
+  else UTV_CHECK(make_map32(&mA, A, M, K, lda, tf32::BM, tf32::BK));
+  // B (op(B) is K x N): !TB -> stored K x N (K contiguous); else N x K (N contiguous)
+  if (!tb) UTV_CHECK(make_map32(&mB, B, K, N, ldb, tf32::BK, tf32::BN));
+  else UTV_CHECK(make_map32(&mB, B, N, K, ldb, tf32::BN, tf32::BK));
+  tf32::Args a;
+  a.M = M; a.N = N; a.K = K;
+  a.tm = ceil_div(M, tf32::BM);
+  a.tn = ceil_div(N, tf32::BN);
+  a.tiles = a.tm * a.tn;
+  a.alpha = alpha; a.beta = beta;
+  a.C = C; a.ldc = ldc;
+  const int grid = a.tiles < num_sms() ? a.tiles : num_sms();
+  ProfScope ps(PROF_GEMM_TF32, 2.0 * M * N * K,
+               4.0 * ((double)M * K + (double)K * N + (beta != 0.0f ? 2.0 : 1.0) * M * N), st);
+  if (!ta && !tb) tf32::sgemm_tf32x3_kernel<false, false><<<grid, tf32::THREADS, tf32::SMEM, st>>>(mA, mB, a);
+  else if (!ta && tb) tf32::sgemm_tf32x3_kernel<false, true><<<grid, tf32::THREADS, tf32::SMEM, st>>>(mA, mB, a);
+  else if (ta && !tb) tf32::sgemm_tf32x3_kernel<true, false><<<grid, tf32::THREADS, tf32::SMEM, st>>>(mA, mB, a);
+  else tf32::sgemm_tf32x3_kernel<true, true><<<grid, tf32::THREADS, tf32::SMEM, st>>>(mA, mB, a);
+  UTV_CUDA(cudaGetLastError());
+  return UTV_OK;
+}
+
+}  // namespace utv

@@ -18,7 +18,8 @@ enum ProfCat {
   PROF_JACOBI = 3,    // Jacobi rounds kernel
   PROF_JFINISH = 4,   // Jacobi finish kernel
   PROF_OPS = 5,       // reductions / structured writes / copies
-  PROF_NCAT = 6
+  PROF_GEMM_TF32 = 6, // 3xTF32 tcgen05 GEMM (flops = 2MNK useful)
+  PROF_NCAT = 7
 };
 struct ProfScope {
   ProfScope(int cat, double flops, double bytes, cudaStream_t st, int launches = 1);
@@ -38,6 +39,10 @@ size_t dgemm_ws_doubles(int M, int N, int K);
 int dgemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, long lda,
           const double* B, long ldb, double beta, double* C, long ldc, double* ws,
           size_t ws_doubles, cudaStream_t st);
+
+// ---- K10 3xTF32 GEMM (gemm_tf32.cu): fp32 operands, ld % 4 == 0, 16B-aligned A/B ----
+int sgemm_tf32x3(bool ta, bool tb, int M, int N, int K, float alpha, const float* A, long lda,
+                 const float* B, long ldb, float beta, float* C, long ldc, cudaStream_t st);
 
 // ---- small device ops (ops.cu) ----
 // out[0] = sum of squares of the rows x cols block (deterministic two-pass).

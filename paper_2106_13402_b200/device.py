@@ -30,6 +30,21 @@ def gemm(transa, transb, alpha, A: DMat, B: DMat, beta=0.0, C: DMat | None = Non
     return C
 
 
+def sgemm_tf32x3(transa, transb, alpha, A: DMat, B: DMat, beta=0.0, C: DMat | None = None):
+    """FP32 GEMM on the tensor cores with the 3xTF32 split (utv_sgemm_tf32x3)."""
+    import torch
+    ta, tb = transa.upper() == "T", transb.upper() == "T"
+    m = A.cols if ta else A.rows
+    k = A.rows if ta else A.cols
+    n = B.rows if tb else B.cols
+    if C is None:
+        C = dempty(m, n, dtype=torch.float32)
+        beta = 0.0
+    check(load().utv_sgemm_tf32x3(transa.encode(), transb.encode(), m, n, k, alpha, A.ptr, A.ld,
+                                  B.ptr, B.ld, beta, C.ptr, C.ld, stream_ptr()), "utv_sgemm_tf32x3")
+    return C
+
+
 def sumsq(A: DMat):
     import torch
     lib = load()
