@@ -114,7 +114,7 @@ int utv_dorgqr(int m, int ncols, int w, const double* Y, long ldy, const double*
 
 /* SVD of an n x n block by one-sided Jacobi: sigma descending, full U, V,
  * reference sign rule.  *status (device int) = sweeps used, -1 = no
- * convergence.  Replaces svd_dense(a, "full") (svd.py:37-58). n <= 400. */
+ * convergence.  Replaces svd_dense(a, "full") (svd.py:37-58). n <= 1024. */
 size_t utv_dgesvj_bufsize(int n);
 int utv_dgesvj(int n, const double* A, long lda, double* sigma, double* U, long ldu, double* V,
                long ldv, int* status, void* work, size_t lwork, void* stream);
@@ -131,6 +131,15 @@ int utv_dgesvj(int n, const double* A, long lda, double* sigma, double* U, long 
 size_t utv_randutv_basic_bufsize(int m, int n, int b, int q);
 int utv_randutv_basic_f64(int m, int n, int b, int q, double* T, long ldt, double* U, long ldu,
                           double* V, long ldv, const double* G, long ldg, double* errsq,
+                          double* trail2, int* svd_status, void* work, size_t lwork,
+                          void* stream);
+
+/* fp32 variant of randutv_basic (BASELINE C5): T, U, V, G fp32; every GEMM
+ * 3xTF32 on tcgen05; panel QRs and the b x b Jacobi SVD in fp64 on converted
+ * panels.  m, n, b and all leading dimensions multiples of 4. */
+size_t utv_randutv_basic_f32_bufsize(int m, int n, int b, int q);
+int utv_randutv_basic_f32(int m, int n, int b, int q, float* T, long ldt, float* U, long ldu,
+                          float* V, long ldv, const float* G, long ldg, double* errsq,
                           double* trail2, int* svd_status, void* work, size_t lwork,
                           void* stream);
 

@@ -46,6 +46,10 @@ SIGNATURES = {
     "utv_randutv_basic_f64": (c_int, [c_int, c_int, c_int, c_int, c_void_p, c_long, c_void_p,
                                       c_long, c_void_p, c_long, c_void_p, c_long, c_void_p,
                                       c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "utv_randutv_basic_f32_bufsize": (c_size_t, [c_int, c_int, c_int, c_int]),
+    "utv_randutv_basic_f32": (c_int, [c_int, c_int, c_int, c_int, c_void_p, c_long, c_void_p,
+                                      c_long, c_void_p, c_long, c_void_p, c_long, c_void_p,
+                                      c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     "utv_powerurv_bufsize": (c_size_t, [c_int, c_int, c_int]),
     "utv_powerurv_f64": (c_int, [c_int, c_int, c_int, c_void_p, c_long, c_void_p, c_long,
                                  c_void_p, c_long, c_void_p, c_long, c_void_p, c_long, c_void_p,

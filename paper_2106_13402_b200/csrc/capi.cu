@@ -9,6 +9,10 @@ size_t randutv_ws_doubles(int m, int n, int b);
 int randutv_basic(int m, int n, int b, int q, Mat T, Mat U, Mat V, const double* G, long ldg,
                   double* errsq, double* trail2, int* svd_status, double* ws, size_t ws_doubles,
                   cudaStream_t st);
+size_t randutv32_ws_bytes(int m, int n, int b);
+int randutv_basic_f32(int m, int n, int b, int q, float* Tp, long ldt, float* Up, long ldu,
+                      float* Vp, long ldv, const float* G, long ldg, double* errsq, double* trail2,
+                      int* svd_status, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t powerurv_ws_doubles(int m, int n);
 int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, Mat Vt, double* ws,
              size_t ws_doubles, cudaStream_t st);
@@ -98,6 +102,21 @@ int utv_dlarfb(char side, char trans, int m, int n, int k, int w, const double* 
 }
 
 int utv_dgeqrf_rows_max(void) { return panel_rows_max(); }
+
+size_t utv_randutv_basic_f32_bufsize(int m, int n, int b, int) { return randutv32_ws_bytes(m, n, b); }
+
+int utv_randutv_basic_f32(int m, int n, int b, int q, float* T, long ldt, float* U, long ldu,
+                          float* V, long ldv, const float* G, long ldg, double* errsq,
+                          double* trail2, int* svd_status, void* work, size_t lwork, void* stream) {
+  if (m < 1 || n < 1) return -1;
+  if (b < 1 || b > 1024) return -3;
+  if (q < 0) return -4;
+  if (ldt < m) return -6;
+  if (ldu < m) return -8;
+  if (ldv < n) return -10;
+  return randutv_basic_f32(m, n, b, q, T, ldt, U, ldu, V, ldv, G, ldg, errsq, trail2, svd_status,
+                           work, lwork, S(stream));
+}
 
 int utv_sgemm_tf32x3(char transa, char transb, int m, int n, int k, float alpha, const float* A,
                      long lda, const float* Bm, long ldb, float beta, float* C, long ldc,
@@ -207,7 +226,7 @@ size_t utv_dgesvj_bufsize(int n) { return B(gesvj_ws_doubles(n)); }
 
 int utv_dgesvj(int n, const double* A, long lda, double* sigma, double* U, long ldu, double* V,
                long ldv, int* status, void* work, size_t lwork, void* stream) {
-  if (n < 1 || n > 400) return -1;
+  if (n < 1 || n > 1024) return -1;
   if (lda < n) return -3;
   if (ldu < n) return -6;
   if (ldv < n) return -8;
@@ -223,7 +242,7 @@ int utv_randutv_basic_f64(int m, int n, int b, int q, double* T, long ldt, doubl
                           void* stream) {
   if (m < 1) return -1;
   if (n < 1 || n > m) return -2;
-  if (b < 1 || b > 400) return -3;
+  if (b < 1 || b > 1024) return -3;
   if (q < 0) return -4;
   if (!ld_ok(ldt, m)) return -6;
   if (!ld_ok(ldu, m)) return -8;

@@ -23,8 +23,7 @@
 namespace utv {
 
 namespace jac {
-constexpr int W = 16;             // columns per block
-constexpr int THREADS = 512;      // 16 warps -> 16 column pairs of a 32-column block pair
+constexpr int WMAX = 16;          // columns per block (16 for n <= 400, 8 up to 800, 4 beyond)
 constexpr int MAX_SWEEPS = 40;
 constexpr double EPS = 2.220446049250313e-16;
 
@@ -101,7 +100,8 @@ __device__ __forceinline__ bool rotate_pair(double* __restrict__ ax, double* __r
 // rotates only the W^2 cross pairs (W sub-rounds of W disjoint pairs, one
 // warp per pair); the intra-block pairs are swept once per sweep in round 0.
 // Sequential sub-rounds per sweep: (W-1) + (2G-1) W  ~ n.
-__global__ void __launch_bounds__(THREADS, 1) jacobi_rounds_kernel(Args a) {
+template <int W>
+__global__ void __launch_bounds__(32 * W, 1) jacobi_rounds_kernel(Args a) {
   extern __shared__ double sm[];
   const int n = a.n;
   const int ldS = n;
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(THREADS, 1) jacobi_rounds_kernel(Args a) {
       round_pair(N, r, g, &bp, &bq);
       // load the two blocks (16-byte vector loads; n is padded to even)
       const int n2 = n >> 1;
-      for (int idx = threadIdx.x; idx < 2 * W * n2; idx += THREADS) {
+      for (int idx = threadIdx.x; idx < 2 * W * n2; idx += 32 * W) {
         const int c = idx / n2, i = (idx - c * n2) * 2;
         const int gc = (c < W ? bp * W + c : bq * W + (c - W));
         const double2 va = __ldcg((const double2*)&a.A[i + (long)gc * a.ld]);
@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(THREADS, 1) jacobi_rounds_kernel(Args a) {
       if ((threadIdx.x & 31) == 0 && nrot) atomicAdd(&s_rot, nrot);
       __syncthreads();
       if (threadIdx.x == 0 && s_rot) atomicAdd(&a.rot[sweep], s_rot);
-      for (int idx = threadIdx.x; idx < 2 * W * n2; idx += THREADS) {
+      for (int idx = threadIdx.x; idx < 2 * W * n2; idx += 32 * W) {
         const int c = idx / n2, i = (idx - c * n2) * 2;
         const int gc = (c < W ? bp * W + c : bq * W + (c - W));
         *(double2*)&a.A[i + (long)gc * a.ld] = *(const double2*)&As[c * ldS + i];
@@ -290,8 +290,17 @@ __global__ void __launch_bounds__(1024) jacobi_finish_kernel(const double* __res
 }
 }  // namespace jac
 
-static inline int jac_blocks(int n) {
-  int nb = (n + jac::W - 1) / jac::W;
+// Column-block width: the resident block pair (A and V, 2W columns each) must
+// fit the 200 KB smem budget: 4 W n 8 bytes.
+static inline int jac_width(int n) {
+  const int ne = n + (n & 1);
+  if ((size_t)4 * 16 * ne * 8 <= 200 * 1024) return 16;
+  if ((size_t)4 * 8 * ne * 8 <= 200 * 1024) return 8;
+  return 4;
+}
+
+static inline int jac_blocks(int n, int W) {
+  int nb = (n + W - 1) / W;
   if (nb & 1) nb++;
   if (nb < 2) nb = 2;
   return nb;
@@ -299,7 +308,8 @@ static inline int jac_blocks(int n) {
 
 size_t gesvj_ws_doubles(int n) {
   const long ld = round_up(n, 4);
-  const long npad = (long)jac_blocks(n) * jac::W;
+  const int W = jac_width(n);
+  const long npad = (long)jac_blocks(n, W) * W;
   return 2 * ld * npad + 2048 + (size_t)jac::MAX_SWEEPS + 64 + 4 * 32;
 }
 
@@ -311,8 +321,9 @@ int gesvj(Mat A, double* sigma, Mat U, Mat V, double* ws, size_t ws_doubles, int
   if (n <= 0) return UTV_OK;
   if (n > 1024) return -1;
   const long ld = round_up(n, 4);
-  const int nblk = jac_blocks(n);
-  const long npad = (long)nblk * jac::W;
+  const int W = jac_width(n);
+  const int nblk = jac_blocks(n, W);
+  const long npad = (long)nblk * W;
   Arena ar{(char*)ws, ws_doubles * sizeof(double), 0};
   double* Aw = ar.take(ld * npad);
   double* Vw = ar.take(ld * npad);
@@ -334,10 +345,10 @@ int gesvj(Mat A, double* sigma, Mat U, Mat V, double* ws, size_t ws_doubles, int
   a.ctr = (unsigned*)(ctl + jac::MAX_SWEEPS);
   a.status = status_dev;
   const int G = nblk / 2;
-  const size_t smem = (size_t)4 * jac::W * ne * sizeof(double);
+  const size_t smem = (size_t)4 * W * ne * sizeof(double);
   if (!g_jac_attr) {
-    UTV_CUDA(cudaFuncSetAttribute(jac::jacobi_rounds_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    for (auto f : {jac::jacobi_rounds_kernel<16>, jac::jacobi_rounds_kernel<8>, jac::jacobi_rounds_kernel<4>})
+      UTV_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     UTV_CUDA(cudaFuncSetAttribute(jac::jacobi_finish_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     g_jac_attr = true;
@@ -345,13 +356,13 @@ int gesvj(Mat A, double* sigma, Mat U, Mat V, double* ws, size_t ws_doubles, int
   if (smem > 200 * 1024) return -1;
   {
   ProfScope ps(PROF_JACOBI, 0.0, 0.0, st);
+  void* kfn = W == 16 ? (void*)jac::jacobi_rounds_kernel<16>
+              : (W == 8 ? (void*)jac::jacobi_rounds_kernel<8> : (void*)jac::jacobi_rounds_kernel<4>);
+  void* args[] = {&a};
   if (G > 1) {
-    void* args[] = {&a};
-    UTV_CUDA(cudaLaunchCooperativeKernel((void*)jac::jacobi_rounds_kernel, dim3(G),
-                                         dim3(jac::THREADS), args, smem, st));
+    UTV_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(32 * W), args, smem, st));
   } else {
-    jac::jacobi_rounds_kernel<<<1, jac::THREADS, smem, st>>>(a);
-    UTV_CUDA(cudaGetLastError());
+    UTV_CUDA(cudaLaunchKernel(kfn, dim3(1), dim3(32 * W), args, smem, st));
   }
   }
   const size_t smem2 = (size_t)4 * (n + 2) * sizeof(double);

@@ -51,6 +51,21 @@ __global__ void sumsq_partial(const double* __restrict__ A, long lda, int rows, 
   if (threadIdx.x == 0) part[blockIdx.x] = acc;
 }
 
+__global__ void sumsq_partial_f32(const float* __restrict__ A, long lda, int rows, int cols,
+                                  double* __restrict__ part) {
+  __shared__ double sh[32];
+  double acc = 0.0;
+  for (int c = blockIdx.x; c < cols; c += gridDim.x) {
+    const float* col = A + (long)c * lda;
+    for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+      const double x = col[r];
+      acc = fma(x, x, acc);
+    }
+  }
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
 __global__ void sum_partials(const double* __restrict__ part, int n, double* out) {
   __shared__ double sh[32];
   double acc = 0.0;
@@ -111,6 +126,45 @@ __global__ void dscale_kernel(double* A, long lda, int rows, int cols, const dou
        i += (long)gridDim.x * blockDim.x) {
     const int r = (int)(i % rows), c = (int)(i / rows);
     A[r + (long)c * lda] *= alpha * d[side == 0 ? r : c];
+  }
+}
+
+template <class S, class D>
+__global__ void cvt_kernel(const S* __restrict__ src, long lds, D* __restrict__ dst, long ldd,
+                           int rows, int cols) {
+  const long total = (long)rows * cols;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total;
+       i += (long)gridDim.x * blockDim.x) {
+    const int r = (int)(i % rows), c = (int)(i / rows);
+    dst[r + (long)c * ldd] = (D)src[r + (long)c * lds];
+  }
+}
+
+__global__ void sumsq_partial_f32(const float* __restrict__ A, long lda, int rows, int cols,
+                                  double* __restrict__ part);
+
+// A (fp32) <- A * 2^-e with 2^e ~ sqrt(*ss): exact rescaling (no rounding),
+// keeps the unstabilised fp32 sampler inside the normal range.
+__global__ void pow2_scale_kernel(float* A, long lda, int rows, int cols, const double* ss) {
+  const double v = *ss;
+  if (!(v > 0.0) || !isfinite(v)) return;
+  int e;
+  frexp(sqrt(v), &e);
+  const float f = ldexpf(1.0f, -e);
+  const long total = (long)rows * cols;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total;
+       i += (long)gridDim.x * blockDim.x) {
+    const int r = (int)(i % rows), c = (int)(i / rows);
+    A[r + (long)c * lda] *= f;
+  }
+}
+
+__global__ void diag_f32_kernel(float* A, long lda, int rows, int cols, const double* d) {
+  const long total = (long)rows * cols;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total;
+       i += (long)gridDim.x * blockDim.x) {
+    const int r = (int)(i % rows), c = (int)(i / rows);
+    A[r + (long)c * lda] = (r == c) ? (float)d[r] : 0.0f;
   }
 }
 
@@ -187,6 +241,56 @@ int set_diag(double* A, long lda, int nr, int nc, const double* d, cudaStream_t 
   if (nr <= 0 || nc <= 0) return UTV_OK;
   ProfScope ps(PROF_OPS, 0.0, 8.0 * nr * nc, st);
   ops::diag_kernel<<<ops::grid_for((long)nr * nc), 256, 0, st>>>(A, lda, nr, nc, d);
+  UTV_CUDA(cudaGetLastError());
+  return UTV_OK;
+}
+
+int sumsq_f32(const float* A, long lda, int rows, int cols, double* out, double* scratch,
+              cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) {
+    UTV_CUDA(cudaMemsetAsync(out, 0, sizeof(double), st));
+    return UTV_OK;
+  }
+  ProfScope ps(PROF_OPS, 2.0 * rows * cols, 4.0 * rows * cols, st, 2);
+  ops::sumsq_partial_f32<<<ops::RED_BLOCKS, ops::RED_THREADS, 0, st>>>(A, lda, rows, cols, scratch);
+  UTV_CUDA(cudaGetLastError());
+  ops::sum_partials<<<1, 512, 0, st>>>(scratch, ops::RED_BLOCKS, out);
+  UTV_CUDA(cudaGetLastError());
+  return UTV_OK;
+}
+
+int cvt_f32_to_f64(const float* src, long lds, double* dst, long ldd, int rows, int cols,
+                   cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return UTV_OK;
+  ProfScope ps(PROF_OPS, 0.0, 12.0 * rows * cols, st);
+  ops::cvt_kernel<float, double><<<ops::grid_for((long)rows * cols), 256, 0, st>>>(src, lds, dst, ldd, rows, cols);
+  UTV_CUDA(cudaGetLastError());
+  return UTV_OK;
+}
+
+int cvt_f64_to_f32(const double* src, long lds, float* dst, long ldd, int rows, int cols,
+                   cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return UTV_OK;
+  ProfScope ps(PROF_OPS, 0.0, 12.0 * rows * cols, st);
+  ops::cvt_kernel<double, float><<<ops::grid_for((long)rows * cols), 256, 0, st>>>(src, lds, dst, ldd, rows, cols);
+  UTV_CUDA(cudaGetLastError());
+  return UTV_OK;
+}
+
+int pow2_normalize_f32(float* A, long lda, int rows, int cols, double* ss, double* scratch,
+                       cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return UTV_OK;
+  UTV_CHECK(sumsq_f32(A, lda, rows, cols, ss, scratch, st));
+  ProfScope ps(PROF_OPS, (double)rows * cols, 8.0 * rows * cols, st);
+  ops::pow2_scale_kernel<<<ops::grid_for((long)rows * cols), 256, 0, st>>>(A, lda, rows, cols, ss);
+  UTV_CUDA(cudaGetLastError());
+  return UTV_OK;
+}
+
+int set_diag_f32(float* A, long lda, int nr, int nc, const double* d, cudaStream_t st) {
+  if (nr <= 0 || nc <= 0) return UTV_OK;
+  ProfScope ps(PROF_OPS, 0.0, 4.0 * nr * nc, st);
+  ops::diag_f32_kernel<<<ops::grid_for((long)nr * nc), 256, 0, st>>>(A, lda, nr, nc, d);
   UTV_CUDA(cudaGetLastError());
   return UTV_OK;
 }

@@ -59,6 +59,16 @@ int laset(int uplo, int rows, int cols, double alpha, double beta, double* A, lo
 // A <- alpha diag(d) A (side 0) or alpha A diag(d) (side 1).
 int diag_scale(int side, int rows, int cols, const double* d, double alpha, double* A, long lda,
                cudaStream_t st);
+// fp32 helpers of the C5 path (ops.cu)
+int sumsq_f32(const float* A, long lda, int rows, int cols, double* out, double* scratch,
+              cudaStream_t st);
+int cvt_f32_to_f64(const float* src, long lds, double* dst, long ldd, int rows, int cols,
+                   cudaStream_t st);
+int cvt_f64_to_f32(const double* src, long lds, float* dst, long ldd, int rows, int cols,
+                   cudaStream_t st);
+int pow2_normalize_f32(float* A, long lda, int rows, int cols, double* ss, double* scratch,
+                       cudaStream_t st);
+int set_diag_f32(float* A, long lda, int nr, int nc, const double* d, cudaStream_t st);
 // diag block: A[:nr, :nc] = 0 except A[i,i] = d[i] (i < min(nr, nc)).
 int set_diag(double* A, long lda, int nr, int nc, const double* d, cudaStream_t st);
 

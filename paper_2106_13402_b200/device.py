@@ -105,15 +105,18 @@ def gesvj(A: DMat):
     return sig, U, V, status
 
 
-def stage_randutv_blocks(blocks, b):
+def stage_randutv_blocks(blocks, b, dtype=None):
     """Concatenate the C-order k_i x b Gaussian draws into one b x sum(k_i)
-    column-major device matrix (block i = G_i^T); ld padded to even."""
+    column-major device matrix (block i = G_i^T); ld padded (even for fp64,
+    a multiple of 4 for fp32)."""
     torch_ = _lib.torch_cuda()
+    dtype = torch_.float64 if dtype is None else dtype
+    npdt = np.float64 if dtype == torch_.float64 else np.float32
     total = sum(int(g.shape[0]) for g in blocks)
-    G = dempty(b, max(total, 1))
+    G = dempty(b, max(total, 1), dtype=dtype)
     col = 0
     for g in blocks:
-        g = np.ascontiguousarray(g, dtype=np.float64)       # C order: rows of length b
+        g = np.ascontiguousarray(g, dtype=npdt)             # C order: rows of length b
         k = g.shape[0]
         G.t[col:col + k, :b].copy_(torch_.from_numpy(g))
         col += k
@@ -142,6 +145,30 @@ class RandUtvRun:
             self.errsq.data_ptr(), self.trail2.data_ptr() if self.trail2 is not None else None,
             self.status.data_ptr(), self.ws.data_ptr(), self.lw, stream_ptr()),
             "utv_randutv_basic_f64")
+
+
+class RandUtvRun32:
+    """fp32 randUTV (3xTF32 tcgen05 GEMMs): workspace + per-step outputs."""
+
+    def __init__(self, m, n, b, q, record_trailing=False):
+        import torch
+        self.m, self.n, self.b, self.q = m, n, b, q
+        lib = load()
+        self.lw = lib.utv_randutv_basic_f32_bufsize(m, n, b, q)
+        self.ws = workspace(self.lw)
+        steps = -(-n // b)
+        self.steps = steps
+        self.errsq = torch.zeros(steps, dtype=torch.float64, device="cuda")
+        self.trail2 = torch.zeros(steps, dtype=torch.float64, device="cuda") if record_trailing else None
+        self.status = torch.zeros(steps, dtype=torch.int32, device="cuda")
+
+    def run(self, T: DMat, U: DMat, V: DMat, G: DMat):
+        lib = load()
+        check(lib.utv_randutv_basic_f32(
+            self.m, self.n, self.b, self.q, T.ptr, T.ld, U.ptr, U.ld, V.ptr, V.ld, G.ptr, G.ld,
+            self.errsq.data_ptr(), self.trail2.data_ptr() if self.trail2 is not None else None,
+            self.status.data_ptr(), self.ws.data_ptr(), self.lw, stream_ptr()),
+            "utv_randutv_basic_f32")
 
 
 class PowerUrvRun:

@@ -28,6 +28,9 @@ class ErrorTracker:
     e_sq: float
     e0_sq: float
     history: list = field(default_factory=list)
+    # randutv.py:55-58 raises below -1e-10 e0^2 (fp64); the fp32 variant's
+    # panel masses carry fp32 rounding, so it uses a fp32-scaled threshold
+    neg_tol: float = 1e-10
 
     @classmethod
     def start(cls, a_fro):
@@ -39,7 +42,7 @@ class ErrorTracker:
 
     def update_mass(self, mass_sq):
         self.e_sq -= float(mass_sq)
-        if self.e_sq < -1e-10 * self.e0_sq:
+        if self.e_sq < -self.neg_tol * self.e0_sq:
             raise ConsistencyError(f"tracked squared error went negative: {self.e_sq:.3e}")
         if self.e_sq < 0.0:
             self.e_sq = 0.0
@@ -107,21 +110,58 @@ def randutv_basic_device(t_dev, b, q, g_dev, record_trailing=False):
     return run, U, V
 
 
-def randutv_basic(a, b, q, rng, record_trailing=False):
-    """Blocked randomized UTV without oversampling (randutv.py:228-235)."""
+def _eye32(n):
+    import torch
+    from ._lib import dempty
+    m = dempty(n, n, dtype=torch.float32)
+    m.t.zero_()
+    idx = torch.arange(n, device="cuda")
+    m.t[idx, idx] = 1.0
+    return m
+
+
+def randutv_basic_device32(t_dev, b, q, g_dev, record_trailing=False):
+    """fp32 device-resident randUTV (BASELINE C5 variant): t_dev (fp32) is
+    overwritten with T; every GEMM is 3xTF32 on the tensor cores."""
+    m, n = t_dev.rows, t_dev.cols
+    run = dv.RandUtvRun32(m, n, b, q, record_trailing)
+    U = _eye32(m)
+    V = _eye32(n)
+    run.run(t_dev, U, V, g_dev)
+    return run, U, V
+
+
+def randutv_basic(a, b, q, rng, record_trailing=False, *, dtype=np.float64):
+    """Blocked randomized UTV without oversampling (randutv.py:228-235).
+
+    dtype=np.float32 selects the fp32 variant (BASELINE C5): T, U, V are
+    computed in fp32 with 3xTF32 tensor-core GEMMs and returned as float32;
+    m, n and b must then be multiples of 4.  The default float64 path is the
+    reference-exact drop-in."""
+    import torch
     a = _validate(a, b, q, 0)
     m, n = a.shape
     b = int(b)
     q = int(q)
+    f32 = np.dtype(dtype) == np.float32
+    if f32 and (m % 4 or n % 4 or b % 4):
+        raise ValueError("the fp32 variant needs m, n and b to be multiples of 4")
     blocks = draw_sample_blocks(rng, m, n, b)
-    t_dev = dfrom_numpy(a)
-    g_dev = dv.stage_randutv_blocks(blocks, b)
-    run, U, V = randutv_basic_device(t_dev, b, q, g_dev, record_trailing)
+    if f32:
+        t_dev = dfrom_numpy(a, dtype=torch.float32)
+        g_dev = dv.stage_randutv_blocks(blocks, b, dtype=torch.float32)
+        run, U, V = randutv_basic_device32(t_dev, b, q, g_dev, record_trailing)
+    else:
+        t_dev = dfrom_numpy(a)
+        g_dev = dv.stage_randutv_blocks(blocks, b)
+        run, U, V = randutv_basic_device(t_dev, b, q, g_dev, record_trailing)
     status = run.status.cpu().numpy()
     if (status < 0).any():
         raise ConvergenceError("b x b Jacobi SVD failed to converge")
     masses = run.errsq.cpu().numpy()
     tracker = ErrorTracker.start(frobenius_norm(a))
+    if f32:
+        tracker.neg_tol = 1e-5
     for mass in masses:
         tracker.update_mass(mass)
     trailing = None
