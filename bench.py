@@ -458,6 +458,112 @@ def run_c4(args):
         torch.distributed.destroy_process_group()
 
 
+# ---------------------------------------------------------------------------
+# C5: fp32 randUTV (3xTF32 tensor cores) on a rank-deficient 32768^2 matrix
+# ---------------------------------------------------------------------------
+
+C5_METRIC = "randUTV b=512 q=2 fp32 (3xTF32 tcgen05), 32768^2 rank 2000: useful TFLOP/s (SURVEY §8d)"
+
+
+def make_rank_deficient_f32(n, r, seed):
+    """A = U_r diag(d) V_r^T, d_i = 10^(-3(i-1)/(r-1)), built on
+    the device with our own QR / GEMM kernels, returned as fp32."""
+    import torch
+    import paper_2106_13402_b200.device as dv
+    from paper_2106_13402_b200._lib import dempty
+    gen = torch.Generator(device="cuda").manual_seed(seed)
+    qs = []
+    for _ in range(2):
+        g = dempty(n, r)
+        g.t.normal_(generator=gen)
+        Y, T = dv.geqrf(g)
+        qs.append(dv.orgqr(Y, T, r))
+        del g, Y, T
+    i = torch.arange(r, device="cuda", dtype=torch.float64)
+    d = 10.0 ** (-3.0 * i / max(r - 1, 1))
+    q1, q2 = qs
+    q1.t[:r, :n].mul_(d[:, None])
+    a64 = dv.gemm("N", "T", 1.0, q1, q2)
+    del q1, q2, qs
+    a = dempty(n, n, dtype=torch.float32)
+    a.t[:, :n].copy_(a64.t[:, :n])
+    del a64
+    torch.cuda.empty_cache()
+    return a
+
+
+def run_c5(args):
+    import torch
+    import paper_2106_13402_b200 as pk
+    import paper_2106_13402_b200.device as dv
+    from paper_2106_13402_b200 import _lib
+    from paper_2106_13402_b200._lib import dempty
+    from paper_2106_13402_b200.randutv import _eye32
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n, b, q, r = args.c5_n, 512, 2, args.c5_rank
+    A = make_rank_deficient_f32(n, r, 50 + rank)
+    blocks = pk.randutv.draw_sample_blocks(pk.RngStream(5), n, n, b)
+    G = dv.stage_randutv_blocks(blocks, b, dtype=torch.float32)
+    del blocks
+    run = dv.RandUtvRun32(n, n, b, q)
+    T = dempty(n, n, dtype=torch.float32)
+    U, V = _eye32(n), _eye32(n)
+    idx = torch.arange(n, device="cuda")
+
+    def step():
+        T.t.copy_(A.t)
+        U.t.zero_(); U.t[idx, idx] = 1.0
+        V.t.zero_(); V.t[idx, idx] = 1.0
+        run.run(T, U, V, G)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    _lib.profile_begin()
+    step()
+    prof = _lib.profile_end()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = _lib.launch_count()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(args.steps):
+        step()
+    t1.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    launches = _lib.launch_count() - launches0
+    secs = t0.elapsed_time(t1) / 1e3
+    if ws > 1:
+        tt = torch.tensor([secs], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        secs = float(tt.item())
+    per = secs / args.steps
+    flops = randutv_flops(n, n, b, q)
+    g = prof["sgemm_tf32x3"]
+    line = {"metric": C5_METRIC, "value": ws * flops / per / 1e12, "unit": "TFLOP/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (3xTF32)",
+            "data": "synthetic rank-deficient (device-generated U_r diag(d) V_r^T; G from the reference PCG64 stream)",
+            "config": {"workload": f"C5 randUTV b={b} q={q} fp32 on {n}x{n}, rank {r}",
+                       "l2_policy": "inputs (4 GiB) larger than L2",
+                       "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
+            "roofline": {"kernel": "sgemm_tf32x3_kernel (tcgen05.mma kind::tf32, 3 products)",
+                         "achieved_useful_tflops": g["flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else 0.0,
+                         "share_of_step": g["ms"] / 1e3 / per},
+            "phase_ms": {k: round(v["ms"], 3) for k, v in prof.items()},
+            "gpu_launches": int(launches), "clocks": clk, "e2e": None, "cpu_baseline": None}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -469,14 +575,19 @@ def main():
     ap.add_argument("--q", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--workload", choices=["headline", "c4"], default="headline",
+    ap.add_argument("--workload", choices=["headline", "c4", "c5"], default="headline",
                     help="headline = BASELINE metric (n=16384 powerURV + randUTV); "
-                         "c4 = row-sharded tall powerURV (BASELINE configs[3])")
+                         "c4 = row-sharded tall powerURV (BASELINE configs[3]); "
+                         "c5 = fp32 3xTF32 randUTV (BASELINE configs[4])")
+    ap.add_argument("--c5-n", type=int, default=32768)
+    ap.add_argument("--c5-rank", type=int, default=2000)
     ap.add_argument("--c4-rows", type=int, default=524288)
     ap.add_argument("--c4-cols", type=int, default=4096)
     args = ap.parse_args()
     if args.workload == "c4" and args.impl != "reference":
         run_c4(args)
+    elif args.workload == "c5" and args.impl != "reference":
+        run_c5(args)
     elif args.impl == "reference":
         run_reference(args)
     else:
