@@ -134,6 +134,19 @@ int utv_randutv_basic_f64(int m, int n, int b, int q, double* T, long ldt, doubl
                           double* trail2, int* svd_status, void* work, size_t lwork,
                           void* stream);
 
+/* One step i (0-based) of blocked randUTV — the host loop of the boosted
+ * (Algorithm 2) and partial variants (randutv_boosted / randutv_partial,
+ * randutv.py:130-139, 196-264), which may stop early on the tracked error.
+ * boosted = 0: basic sampler (G = this step's b x k_i block).  boosted = 1:
+ * oversampled sampler with recycling; G = (b+p) x m at i = 0, b x k_i after.
+ * *carried (host, in/out): carried columns of the recycled block (0 at i=0).
+ * *is_final (host, out): 1 when the step was the final dense SVD. */
+size_t utv_randutv_step_bufsize(int m, int n, int b, int p, int q);
+int utv_randutv_step_f64(int i, int m, int n, int b, int p, int q, int boosted, double* T, long ldt,
+                         double* U, long ldu, double* V, long ldv, const double* G, long ldg,
+                         double* errsq, double* trail2, int* svd_status, int* carried,
+                         int* is_final, void* work, size_t lwork, void* stream);
+
 /* fp32 variant of randutv_basic (BASELINE C5): T, U, V, G fp32; every GEMM
  * 3xTF32 on tcgen05; panel QRs and the b x b Jacobi SVD in fp64 on converted
  * panels.  m, n, b and all leading dimensions multiples of 4. */

@@ -46,6 +46,11 @@ SIGNATURES = {
     "utv_randutv_basic_f64": (c_int, [c_int, c_int, c_int, c_int, c_void_p, c_long, c_void_p,
                                       c_long, c_void_p, c_long, c_void_p, c_long, c_void_p,
                                       c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "utv_randutv_step_bufsize": (c_size_t, [c_int, c_int, c_int, c_int, c_int]),
+    "utv_randutv_step_f64": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p,
+                                     c_long, c_void_p, c_long, c_void_p, c_long, c_void_p, c_long,
+                                     c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                     c_size_t, c_void_p]),
     "utv_randutv_basic_f32_bufsize": (c_size_t, [c_int, c_int, c_int, c_int]),
     "utv_randutv_basic_f32": (c_int, [c_int, c_int, c_int, c_int, c_void_p, c_long, c_void_p,
                                       c_long, c_void_p, c_long, c_void_p, c_long, c_void_p,

@@ -9,6 +9,10 @@ size_t randutv_ws_doubles(int m, int n, int b);
 int randutv_basic(int m, int n, int b, int q, Mat T, Mat U, Mat V, const double* G, long ldg,
                   double* errsq, double* trail2, int* svd_status, double* ws, size_t ws_doubles,
                   cudaStream_t st);
+size_t randutv_ws_doubles_p(int m, int n, int b, int p);
+int randutv_step(int i, int m, int n, int b, int p, int q, bool boosted, Mat T, Mat U, Mat V,
+                 const double* G, long ldg, double* errsq, double* trail2, int* svd_status,
+                 double* ws, size_t ws_doubles, int* carried, int* is_final, cudaStream_t st);
 size_t randutv32_ws_bytes(int m, int n, int b);
 int randutv_basic_f32(int m, int n, int b, int q, float* Tp, long ldt, float* Up, long ldu,
                       float* Vp, long ldv, const float* G, long ldg, double* errsq, double* trail2,
@@ -102,6 +106,26 @@ int utv_dlarfb(char side, char trans, int m, int n, int k, int w, const double* 
 }
 
 int utv_dgeqrf_rows_max(void) { return panel_rows_max(); }
+
+size_t utv_randutv_step_bufsize(int m, int n, int b, int p, int) { return B(randutv_ws_doubles_p(m, n, b, p)); }
+
+int utv_randutv_step_f64(int i, int m, int n, int b, int p, int q, int boosted, double* T, long ldt,
+                         double* U, long ldu, double* V, long ldv, const double* G, long ldg,
+                         double* errsq, double* trail2, int* svd_status, int* carried,
+                         int* is_final, void* work, size_t lwork, void* stream) {
+  if (i < 0 || (long)i * b >= n) return -1;
+  if (m < n || n < 1) return -2;
+  if (b < 1 || b + p > 1024) return -4;
+  if (p < 0) return -5;
+  if (q < 0 || (boosted && q < 1)) return -6;
+  if (!ld_ok(ldt, m)) return -9;
+  if (!ld_ok(ldu, m)) return -11;
+  if (!ld_ok(ldv, n)) return -13;
+  if (!carried || !is_final) return -19;
+  return randutv_step(i, m, n, b, boosted ? p : 0, q, boosted != 0, Mat{T, ldt, m, n},
+                      Mat{U, ldu, m, m}, Mat{V, ldv, n, n}, G, ldg, errsq, trail2, svd_status,
+                      (double*)work, lwork / sizeof(double), carried, is_final, S(stream));
+}
 
 size_t utv_randutv_basic_f32_bufsize(int m, int n, int b, int) { return randutv32_ws_bytes(m, n, b); }
 

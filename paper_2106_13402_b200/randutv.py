@@ -174,11 +174,80 @@ def randutv_basic(a, b, q, rng, record_trailing=False, *, dtype=np.float64):
         errors=list(tracker.history), trailing_fro=trailing)
 
 
+def _randutv_stepwise(a, b, q, p, rng, boosted, tol_fro=None, max_rank=None,
+                      record_trailing=False):
+    """Host step loop over utv_randutv_step_f64 (randutv.py:110-182): the
+    Gaussian block of each step is drawn right before the step, so the
+    caller's rng advances exactly as in the reference even when the run stops
+    early (tol_fro / max_rank, randutv.py:123-124,162-163)."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    a = _validate(a, b, q, p)
+    m, n = a.shape
+    b, q, p = int(b), int(q), int(p)
+    lib = _lib.load()
+    pe = p if boosted else 0
+    if b + pe > 1024:
+        raise ValueError(f"b + p must be <= 1024 on the B200 path, got {b + pe}")
+    t_dev = dfrom_numpy(a)
+    U, V = deye(m), deye(n)
+    steps_max = -(-n // b)
+    errsq = torch.zeros(steps_max, dtype=torch.float64, device="cuda")
+    trail2 = torch.zeros(steps_max, dtype=torch.float64, device="cuda") if record_trailing else None
+    status = torch.zeros(steps_max, dtype=torch.int32, device="cuda")
+    lw = lib.utv_randutv_step_bufsize(m, n, b, pe, q)
+    ws = _lib.workspace(lw)
+    carried, is_final = ctypes.c_int(0), ctypes.c_int(0)
+    tracker = ErrorTracker.start(frobenius_norm(a))
+    trailing = [] if record_trailing else None
+    steps = 0
+    for i in range(1, steps_max + 1):
+        if tol_fro is not None and tracker.e <= tol_fro:
+            break
+        lo = (i - 1) * b
+        ncols = n - lo
+        g_dev = None
+        if ncols > b + pe:
+            rows, cols = (m, b + pe) if (boosted and i == 1) else (m - lo, b)
+            g_dev = dv.stage_randutv_blocks([np.asarray(rng.standard_normal(rows, cols))], cols)
+        check = _lib.check
+        check(lib.utv_randutv_step_f64(
+            i - 1, m, n, b, pe, q, 1 if boosted else 0, t_dev.ptr, t_dev.ld, U.ptr, U.ld, V.ptr, V.ld,
+            g_dev.ptr if g_dev is not None else None, g_dev.ld if g_dev is not None else 2,
+            errsq.data_ptr(), trail2.data_ptr() if trail2 is not None else None, status.data_ptr(),
+            ctypes.byref(carried), ctypes.byref(is_final), ws.data_ptr(), lw, _lib.stream_ptr()),
+            "utv_randutv_step_f64")
+        steps = i
+        if int(status[i - 1].item()) < 0:
+            raise ConvergenceError("b x b Jacobi SVD failed to converge")
+        tracker.update_mass(float(errsq[i - 1].item()))
+        if trailing is not None:
+            trailing.append(0.0 if is_final.value else float(math.sqrt(max(float(trail2[i - 1].item()), 0.0))))
+        if is_final.value:
+            break
+        if max_rank is not None and i * b >= max_rank:
+            break
+    return UtvFactorization(
+        U=np.asfortranarray(U.to_numpy()), T=np.asfortranarray(t_dev.to_numpy()),
+        V=np.asfortranarray(V.to_numpy()), b=b, steps_done=steps, oversample=p, power=q,
+        errors=list(tracker.history), trailing_fro=trailing)
+
+
 def randutv_boosted(a, b, q, p, rng, record_trailing=False):
-    """Algorithm 2 (randutv.py:238-247) — next row of the build plan."""
-    raise NotImplementedError("randutv_boosted is not on the B200 path yet (SURVEY.md §8f row 1)")
+    """Algorithm 2: oversampling + sample recycling (randutv.py:238-247)."""
+    if q < 1:
+        raise ValueError(f"randutv_boosted requires q >= 1, got {q}")
+    return _randutv_stepwise(a, b, q, p, rng, boosted=True, record_trailing=record_trailing)
 
 
 def randutv_partial(a, b, q, p, rng, tol_fro=None, max_rank=None, record_trailing=False):
-    """Partial boosted randUTV (randutv.py:250-264) — next row."""
-    raise NotImplementedError("randutv_partial is not on the B200 path yet (SURVEY.md §8f row 1)")
+    """Boosted randUTV halted by error tolerance or column budget (randutv.py:250-264)."""
+    if q < 1:
+        raise ValueError(f"randutv_partial requires q >= 1, got {q}")
+    if tol_fro is None and max_rank is None:
+        raise ValueError("randutv_partial needs tol_fro or max_rank")
+    return _randutv_stepwise(a, b, q, p, rng, boosted=True, tol_fro=tol_fro, max_rank=max_rank,
+                             record_trailing=record_trailing)

@@ -109,6 +109,46 @@ def main():
              steps=f.steps_done, efro=uk.bench.trailing_fro_curve(f.T),
              call=f"randutv_basic(A,{b},{qq},RngStream({seed}),record_trailing=True)")
 
+    boosted(uk, save)
+
+
+def boosted(uk=None, save=None):
+    """randutv_boosted / randutv_partial (randutv.py:130-139, 196-264)."""
+    if uk is None:
+        sys.dont_write_bytecode = True
+        sys.path.insert(0, REF)
+        import utvkit as uk  # noqa: E402
+
+        def save(name, **kw):
+            path = os.path.join(OUT, name + ".npz")
+            np.savez_compressed(path, **kw)
+            print("wrote", path, os.path.getsize(path), "bytes")
+    cases = []
+    cases.append(("gauss150x100_b30_q1_p30", uk.gaussian(150, 100, uk.RngStream(51)), 30, 1, 30, 52, None, None))
+    fd, _ = uk.gen_fast_decay(200, 1e-5, uk.RngStream(53))
+    cases.append(("fast200_b50_q2_p20", fd, 50, 2, 20, 54, None, None))
+    cases.append(("tall300x260_b64_q2_p64", uk.gaussian(300, 260, uk.RngStream(55)), 64, 2, 64, 56, None, None))
+    cases.append(("gauss160_b32_q1_p0", uk.gaussian(160, 160, uk.RngStream(57)), 32, 1, 0, 58, None, None))
+    cases.append(("gauss96_b40_q1_p16", uk.gaussian(96, 96, uk.RngStream(59)), 40, 1, 16, 60, None, None))
+    cases.append(("partial_rank_tall300x260_b64_q1_p16", uk.gaussian(300, 260, uk.RngStream(61)), 64, 1, 16, 62, None, 100))
+    cases.append(("partial_tol_fast200_b32_q2_p8", fd, 32, 2, 8, 63, 1e-3, None))
+    for key, a, b, qq, pp, seed, tol, mr in cases:
+        rng = uk.RngStream(seed)
+        if key.startswith("partial"):
+            f = uk.randutv_partial(a, b, qq, pp, rng, tol_fro=tol, max_rank=mr, record_trailing=True)
+            call = f"randutv_partial(A,{b},{qq},{pp},RngStream({seed}),tol_fro={tol},max_rank={mr},record_trailing=True)"
+        else:
+            f = uk.randutv_boosted(a, b, qq, pp, rng, record_trailing=True)
+            call = f"randutv_boosted(A,{b},{qq},{pp},RngStream({seed}),record_trailing=True)"
+        nxt = rng.standard_normal(1, 1)[0, 0]      # rng consumption parity
+        save("boost_" + key, A=a, b=b, q=qq, p=pp, seed=seed, tol=np.nan if tol is None else tol,
+             max_rank=-1 if mr is None else mr, U=f.U, T=f.T, V=f.V, errors=np.array(f.errors),
+             trailing=np.array(f.trailing_fro), steps=f.steps_done,
+             efro=uk.bench.trailing_fro_curve(f.T), next_normal=nxt, call=call)
+
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "boosted":
+        boosted()
+    else:
+        main()
