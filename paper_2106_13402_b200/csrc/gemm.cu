@@ -64,6 +64,7 @@ struct Args {
   double* C;
   long ldc;
   double* ws;  // split-K partials [split][N][M] (ld = M)
+  int* sched;  // dynamic tile scheduler [ticket, done] (self-resetting), or null = static
 };
 
 // Physical double offset inside a 128B-swizzled tile whose 128-byte line is
@@ -155,18 +156,56 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   __syncthreads();
 
+  // ---- tile scheduling ----
+  // Dynamic: thread 0 takes tickets from a global counter (the last CTA to
+  // run dry resets it for the next launch on the stream), so CTAs that start
+  // late — their SM held by a concurrent kernel on another stream — simply
+  // find the work done.  Tile ids travel to the consumers through a smem ring
+  // published before the first TMA (or sentinel arrive) of each tile.
+  __shared__ int tq[8];
+  int pseq = 0;  // tiles started by the producer
+  auto next_tile = [&](int prev) -> int {
+    if (!p.sched) {
+      const int t = prev < 0 ? (int)blockIdx.x : prev + (int)gridDim.x;
+      return t < p.tiles ? t : -1;
+    }
+    const int t = atomicAdd(p.sched, 1);
+    if (t < p.tiles) return t;
+    if (atomicAdd(p.sched + 1, 1) == (int)gridDim.x - 1) {
+      atomicExch(p.sched, 0);
+      atomicExch(p.sched + 1, 0);
+    }
+    return -1;
+  };
   // ---- producer state (thread 0 only) ----
-  int ptile = blockIdx.x, pit = 0, pnk = 0;
+  int ptile = -1, pit = 0, pnk = 0;
   long pg = 0;  // global produced k-block count
   TileCoord pc{};
-  if (threadIdx.x == 0 && ptile < p.tiles) {
-    pc = tile_of(p, ptile);
-    pnk = nk_of(pc.z);
+  bool pdone = false;
+  if (threadIdx.x == 0) {
+    ptile = next_tile(-1);
+    if (ptile >= 0) {
+      pc = tile_of(p, ptile);
+      pnk = nk_of(pc.z);
+    }
   }
   auto produce_one = [&]() {
+    if (pdone) return;
+    if (ptile < 0) {
+      // sentinel: publish -1 and complete the slot's phase without data
+      const int s = (int)(pg % STAGES);
+      if (pg >= STAGES) mbar_wait(empty0 + 8 * s, (uint32_t)(((pg / STAGES) & 1) ^ 1));
+      tq[pseq & 7] = -1;
+      ++pseq;
+      mbar_arrive(full0 + 8 * s);
+      ++pg;
+      pdone = true;
+      return;
+    }
     const int s = (int)(pg % STAGES);
     if (pg >= STAGES) mbar_wait(empty0 + 8 * s, (uint32_t)(((pg / STAGES) & 1) ^ 1));
     const uint32_t fb = full0 + 8 * s;
+    if (pit == 0) tq[(pseq++) & 7] = ptile;
     mbar_arrive_expect_tx(fb, STAGE_BYTES);
     const int k = pc.z * p.k_split + pit * BK;  // k' (even)
     const uint32_t dA = smem_u32(sA + s * A_ST), dB = smem_u32(sB + s * B_ST);
@@ -189,8 +228,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     ++pg;
     if (++pit == pnk) {
       pit = 0;
-      ptile += gridDim.x;
-      if (ptile < p.tiles) {
+      ptile = next_tile(ptile);
+      if (ptile >= 0) {
         pc = tile_of(p, ptile);
         pnk = nk_of(pc.z);
       }
@@ -207,8 +246,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    if (HASC && blockIdx.x < p.tiles) load_c(blockIdx.x);
-    for (int i = 0; i < STAGES - 1 && ptile < p.tiles; ++i) produce_one();
+    if (HASC && ptile >= 0) load_c(ptile);
+    for (int i = 0; i < STAGES - 1; ++i) produce_one();
   }
 
   const int wm = warp & 1, wn = warp >> 1;
@@ -220,8 +259,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   for (int u = 0; u < 4; ++u) bcol[u] = frag_col<TB>(wn, u, fr);
 
   long g = 0;   // global consumed k-block count
-  int local = 0;
-  for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x, ++local) {
+  for (int local = 0;; ++local) {
+    // the first stage of the tile publishes its id (or the -1 sentinel)
+    if (threadIdx.x == 0 && pg < g + STAGES) produce_one();
+    __syncwarp();
+    mbar_wait(full0 + 8 * (int)(g % STAGES), (uint32_t)((g / STAGES) & 1));
+    const int tile = tq[local & 7];
+    if (tile < 0) break;
     const TileCoord tc = tile_of(p, tile);
     const int nk = nk_of(tc.z);
     double acc[8][4][2];
@@ -232,7 +276,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     const bool zero_k0 = (p.k_sh != 0) && (tc.z == 0);
     for (int it = 0; it < nk; ++it, ++g) {
-      if (threadIdx.x == 0 && pg < g + STAGES && ptile < p.tiles) produce_one();
+      if (threadIdx.x == 0 && it > 0 && pg < g + STAGES) produce_one();
       __syncwarp();
       const int s = (int)(g % STAGES);
       mbar_wait(full0 + 8 * s, (uint32_t)((g / STAGES) & 1));
@@ -286,7 +330,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     if (HASC) {
       __syncthreads();  // every warp is done with sC
-      if (threadIdx.x == 0 && tile + (int)gridDim.x < p.tiles) load_c(tile + gridDim.x);
+      if (threadIdx.x == 0) {
+        const int nxt = tq[(local + 1) & 7];  // published: the producer runs >= 1 k-block ahead
+        if (nxt >= 0) load_c(nxt);
+      }
     }
   }
 }
@@ -356,6 +403,30 @@ int num_sms() {
   get_encode();
   return g_num_sms > 0 ? g_num_sms : 148;
 }
+
+// ---- dynamic tile scheduler slots: one [ticket, done] pair per stream ----
+static std::mutex g_sched_mu;
+static int* g_sched = nullptr;
+static cudaStream_t g_sched_streams[64];
+static int g_sched_n = 0;
+
+static int* sched_slot(cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_sched_mu);
+  if (!g_sched) {
+    if (cudaMalloc((void**)&g_sched, 2 * 64 * sizeof(int)) != cudaSuccess) return nullptr;
+    if (cudaMemset(g_sched, 0, 2 * 64 * sizeof(int)) != cudaSuccess) return nullptr;
+  }
+  for (int i = 0; i < g_sched_n; ++i)
+    if (g_sched_streams[i] == st) return g_sched + 2 * i;
+  if (g_sched_n == 64) return nullptr;  // fall back to static scheduling
+  g_sched_streams[g_sched_n] = st;
+  return g_sched + 2 * (g_sched_n++);
+}
+
+// CTA budget of the next GEMM launches on this host thread (0 = all SMs):
+// drivers lower it while a latency-bound kernel runs on a side stream.
+static thread_local int g_max_ctas = 0;
+void gemm_set_max_ctas(int n) { g_max_ctas = n; }
 
 // Tensor map over a column-major (rows x cols) matrix with leading dim ld.
 // TMA needs a 16B-aligned origin and 16B-aligned box starts in dim0, so an
@@ -539,7 +610,10 @@ int dgemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, 
   a.alpha = alpha; a.beta = beta;
   a.C = C; a.ldc = ldc;
   a.ws = use_ws ? ws : nullptr;
-  const int grid = a.tiles < num_sms() ? a.tiles : num_sms();
+  a.sched = sched_slot(st);
+  int cap = num_sms();
+  if (g_max_ctas > 0 && g_max_ctas < cap) cap = g_max_ctas;
+  const int grid = a.tiles < cap ? a.tiles : cap;
   {
   ProfScope ps(PROF_GEMM, 2.0 * M * N * K, 8.0 * ((double)M * K + (double)K * N + (beta != 0.0 ? 2.0 : 1.0) * M * N), st);
   if (hasc) {
