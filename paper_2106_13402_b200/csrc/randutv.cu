@@ -13,6 +13,8 @@
 // on the tracked error, randutv.py:123-124).  The boosted sampler's carried
 // columns (w_next, randutv.py:135-138) live in the caller's workspace
 // between steps.
+#include <mutex>
+
 #include "common.cuh"
 #include "utv_internal.h"
 
@@ -162,6 +164,43 @@ static int boosted_right_basis(int i, Mat Bk, int b, int p, int q, const double*
   return UTV_OK;
 }
 
+// ---- phases of a regular step (lo = i b, k = m - lo, kc = n - lo) ----
+// front_b: right transform (randutv.py:143-144) and the T-panel QR (:146).
+static int front_b(int lo, Mat T, Mat U, Mat V, Mat Yv, Mat Tv, int k, int kc, int b,
+                   const RutvWs& w, cudaStream_t st) {
+  const int m = T.rows, n = V.rows;
+  UTV_CHECK(larfb('R', false, Yv, Tv, T.sub(0, lo, m, kc), w.lfb, w.lfb_n, st));
+  UTV_CHECK(larfb('R', false, Yv, Tv, V.sub(0, lo, n, kc), w.lfb, w.lfb_n, st));
+  Mat Yu{w.Yu, w.ldm, k, b}, Tu{w.Tu, w.ldb, b, b};
+  return geqrf(T.sub(lo, lo, k, b), Yu, Tu, true, w.qr, w.qr_n, st);
+}
+// front_c: left transform (randutv.py:147-149); T[mid:, lo:mid] is already
+// exactly zero (geqrf writes R with zeros below).
+static int front_c(int lo, Mat T, Mat U, int k, int kc, int b, const RutvWs& w, cudaStream_t st) {
+  const int m = T.rows, mid = lo + b;
+  Mat Yu{w.Yu, w.ldm, k, b}, Tu{w.Tu, w.ldb, b, b};
+  UTV_CHECK(larfb('R', false, Yu, Tu, U.sub(0, lo, m, k), w.lfb, w.lfb_n, st));
+  return larfb('L', true, Yu, Tu, T.sub(lo, mid, k, kc - b), w.lfb, w.lfb_n, st);
+}
+// step_svd: b x b SVD of R = T[lo:mid, lo:mid] (randutv.py:151).
+static int step_svd(int lo, Mat T, int b, int* status, const RutvWs& w, cudaStream_t st) {
+  return gesvj(T.sub(lo, lo, b, b), w.sig, Mat{w.Us, w.ldb, b, b}, Mat{w.Vs, w.ldb, b, b}, w.svd,
+               w.svd_n, status, st);
+}
+// step_back: rotations, diag(sigma), error tracking (randutv.py:152-161).
+static int step_back(int i, int lo, Mat T, Mat U, Mat V, int m, int n, int kc, int b, double* errsq,
+                     double* trail2, const RutvWs& w, cudaStream_t st) {
+  const int mid = lo + b;
+  UTV_CHECK(rotate_right(U.sub(0, lo, m, b), w.Us, w.ldb, b, w, st));
+  UTV_CHECK(rotate_right(V.sub(0, lo, n, b), w.Vs, w.ldb, b, w, st));
+  UTV_CHECK(set_diag(T.at(lo, lo), T.ld, b, b, w.sig, st));
+  UTV_CHECK(rotate_left_t(T.sub(lo, mid, b, kc - b), w.Us, w.ldb, b, w, st));
+  UTV_CHECK(rotate_right(T.sub(0, lo, lo, b), w.Vs, w.ldb, b, w, st));
+  UTV_CHECK(sumsq(T.at(lo, lo), T.ld, b, kc, errsq + i, w.red, st));
+  if (trail2) UTV_CHECK(sumsq(T.at(mid, mid), T.ld, m - mid, kc - b, trail2 + i, w.red, st));
+  return UTV_OK;
+}
+
 // One step i (0-based) of randUTV.  G: this step's Gaussian block (transposed
 // C-order draw).  p = 0 and boosted = false is the basic variant.  *is_final
 // is set when the step was the final dense-SVD step; *carried (host) is the
@@ -196,26 +235,10 @@ int randutv_step(int i, int m, int n, int b, int p, int q, bool boosted, Mat T, 
       UTV_CHECK(sample_basic(Bk, b, q, G, ldg, w, st));
       UTV_CHECK(geqrf(Mat{w.Y, w.ldn, kc, b}, Yv, Tv, true, w.qr, w.qr_n, st));
     }
-    // ---- right transform (randutv.py:143-144) ----
-    UTV_CHECK(larfb('R', false, Yv, Tv, T.sub(0, lo, m, kc), w.lfb, w.lfb_n, st));
-    UTV_CHECK(larfb('R', false, Yv, Tv, V.sub(0, lo, n, kc), w.lfb, w.lfb_n, st));
-    // ---- left transform: [Uq, R] = hqr_full(T[lo:, lo:mid]) (randutv.py:146-149) ----
-    Mat Yu{w.Yu, w.ldm, k, b}, Tu{w.Tu, w.ldb, b, b};
-    UTV_CHECK(geqrf(T.sub(lo, lo, k, b), Yu, Tu, true, w.qr, w.qr_n, st));
-    UTV_CHECK(larfb('R', false, Yu, Tu, U.sub(0, lo, m, k), w.lfb, w.lfb_n, st));
-    UTV_CHECK(larfb('L', true, Yu, Tu, T.sub(lo, mid, k, kc - b), w.lfb, w.lfb_n, st));
-    // T[mid:, lo:mid] is already exactly zero (geqrf writes R with zeros below).
-    // ---- b x b SVD and rotations (randutv.py:151-156) ----
-    Mat Us{w.Us, w.ldb, b, b}, Vs{w.Vs, w.ldb, b, b};
-    UTV_CHECK(gesvj(T.sub(lo, lo, b, b), w.sig, Us, Vs, w.svd, w.svd_n, svd_status + i, st));
-    UTV_CHECK(rotate_right(U.sub(0, lo, m, b), w.Us, w.ldb, b, w, st));
-    UTV_CHECK(rotate_right(V.sub(0, lo, n, b), w.Vs, w.ldb, b, w, st));
-    UTV_CHECK(set_diag(T.at(lo, lo), T.ld, b, b, w.sig, st));
-    UTV_CHECK(rotate_left_t(T.sub(lo, mid, b, kc - b), w.Us, w.ldb, b, w, st));
-    UTV_CHECK(rotate_right(T.sub(0, lo, lo, b), w.Vs, w.ldb, b, w, st));
-    // ---- error tracking (randutv.py:159-161) ----
-    UTV_CHECK(sumsq(T.at(lo, lo), T.ld, b, kc, errsq + i, w.red, st));
-    if (trail2) UTV_CHECK(sumsq(T.at(mid, mid), T.ld, m - mid, kc - b, trail2 + i, w.red, st));
+    UTV_CHECK(front_b(lo, T, U, V, Yv, Tv, k, kc, b, w, st));
+    UTV_CHECK(front_c(lo, T, U, k, kc, b, w, st));
+    UTV_CHECK(step_svd(lo, T, b, svd_status + i, w, st));
+    UTV_CHECK(step_back(i, lo, T, U, V, m, n, kc, b, errsq, trail2, w, st));
     return UTV_OK;
   }
   *is_final = 1;
@@ -238,6 +261,34 @@ int randutv_step(int i, int m, int n, int b, int p, int q, bool boosted, Mat T, 
   return UTV_OK;
 }
 
+// Side stream for the latency-bound b x b Jacobi SVD (created once, high
+// priority so its few CTAs are dispatched ahead of the GEMM tiles).
+static int side_stream(cudaStream_t* s1, cudaEvent_t* ev) {
+  static cudaStream_t g_s1 = nullptr;
+  static cudaEvent_t g_ev[2];
+  static std::once_flag once;
+  static int err = 0;
+  std::call_once(once, [] {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&g_s1, cudaStreamNonBlocking, hi) != cudaSuccess) err = 1;
+    for (int e = 0; e < 2; ++e)
+      if (cudaEventCreateWithFlags(&g_ev[e], cudaEventDisableTiming) != cudaSuccess) err = 1;
+  });
+  if (err) return UTV_ERR_CUDA;
+  *s1 = g_s1;
+  ev[0] = g_ev[0];
+  ev[1] = g_ev[1];
+  return UTV_OK;
+}
+
+// Whole basic loop, software-pipelined over two streams: the Jacobi SVD of
+// step i runs on the side stream while the main stream proceeds with the
+// left transform of step i and the sampling + Y-panel QR of step i+1; the
+// rotations of step i follow on the main stream just before step i+1's
+// right transform (the first operation that touches rows lo:mid of T
+// again).  Data dependencies are unchanged, so results are bitwise the same
+// as the one-stream step sequence.
 int randutv_basic(int m, int n, int b, int q, Mat T, Mat U, Mat V, const double* G, long ldg,
                   double* errsq, double* trail2, int* svd_status, double* ws, size_t ws_doubles,
                   cudaStream_t st) {
@@ -245,16 +296,50 @@ int randutv_basic(int m, int n, int b, int q, Mat T, Mat U, Mat V, const double*
   if (b < 1) return -3;
   if (q < 0) return -4;
   if (ws_doubles < plan_rutv(m, n, b, -1, nullptr, nullptr)) return UTV_ERR_WORKSPACE;
+  RutvWs w;
+  plan_rutv(m, n, b, -1, &w, ws);
+  cudaStream_t s1;
+  cudaEvent_t ev[2];  // [0] R ready (main), [1] SVD done (side)
+  UTV_CHECK(side_stream(&s1, ev));
   const int nsteps = (n + b - 1) / b;
   long gcol = 0;
-  int carried = 0;
+  int pending = -1;  // step whose SVD is in flight on the side stream
   for (int i = 0; i < nsteps; ++i) {
-    const int k = m - i * b;
-    int fin = 0;
-    UTV_CHECK(randutv_step(i, m, n, b, 0, q, false, T, U, V, G + gcol * ldg, ldg, errsq, trail2,
-                           svd_status, ws, ws_doubles, &carried, &fin, st));
-    if (fin) break;
+    const int lo = i * b;
+    const int k = m - lo, kc = n - lo;
+    if (kc <= b) {
+      if (pending >= 0) {
+        UTV_CUDA(cudaStreamWaitEvent(st, ev[1], 0));
+        UTV_CHECK(step_back(pending, pending * b, T, U, V, m, n, n - pending * b, b, errsq, trail2, w, st));
+        pending = -1;
+      }
+      int carried = 0, fin = 0;
+      UTV_CHECK(randutv_step(i, m, n, b, 0, q, false, T, U, V, nullptr, ldg, errsq, trail2,
+                             svd_status, ws, ws_doubles, &carried, &fin, st));
+      break;
+    }
+    Mat Bk = T.sub(lo, lo, k, kc);
+    Mat Yv{w.Yv, w.ldn, kc, b}, Tv{w.Tv, w.ldb, b, b};
+    // front_a: sampling (randutv.py:185-193) + [Vq, ~] = hqr_full(Y) (:141)
+    UTV_CHECK(sample_basic(Bk, b, q, G + gcol * ldg, ldg, w, st));
+    UTV_CHECK(geqrf(Mat{w.Y, w.ldn, kc, b}, Yv, Tv, true, w.qr, w.qr_n, st));
     gcol += k;
+    if (pending >= 0) {
+      UTV_CUDA(cudaStreamWaitEvent(st, ev[1], 0));
+      UTV_CHECK(step_back(pending, pending * b, T, U, V, m, n, n - pending * b, b, errsq, trail2, w, st));
+      pending = -1;
+    }
+    UTV_CHECK(front_b(lo, T, U, V, Yv, Tv, k, kc, b, w, st));
+    UTV_CUDA(cudaEventRecord(ev[0], st));
+    UTV_CUDA(cudaStreamWaitEvent(s1, ev[0], 0));
+    UTV_CHECK(step_svd(lo, T, b, svd_status + i, w, s1));
+    UTV_CUDA(cudaEventRecord(ev[1], s1));
+    pending = i;
+    UTV_CHECK(front_c(lo, T, U, k, kc, b, w, st));
+  }
+  if (pending >= 0) {
+    UTV_CUDA(cudaStreamWaitEvent(st, ev[1], 0));
+    UTV_CHECK(step_back(pending, pending * b, T, U, V, m, n, n - pending * b, b, errsq, trail2, w, st));
   }
   return UTV_OK;
 }
