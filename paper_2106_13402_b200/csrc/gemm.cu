@@ -410,7 +410,7 @@ static int* g_sched = nullptr;
 static cudaStream_t g_sched_streams[64];
 static int g_sched_n = 0;
 
-static int* sched_slot(cudaStream_t st) {
+int* gemm_sched_slot(cudaStream_t st) {
   std::lock_guard<std::mutex> lk(g_sched_mu);
   if (!g_sched) {
     if (cudaMalloc((void**)&g_sched, 2 * 64 * sizeof(int)) != cudaSuccess) return nullptr;
@@ -610,7 +610,7 @@ int dgemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, 
   a.alpha = alpha; a.beta = beta;
   a.C = C; a.ldc = ldc;
   a.ws = use_ws ? ws : nullptr;
-  a.sched = sched_slot(st);
+  a.sched = gemm_sched_slot(st);
   int cap = num_sms();
   if (g_max_ctas > 0 && g_max_ctas < cap) cap = g_max_ctas;
   const int grid = a.tiles < cap ? a.tiles : cap;

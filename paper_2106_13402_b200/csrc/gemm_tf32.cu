@@ -41,7 +41,7 @@ constexpr int EPI_WARP0 = 12;                 // epilogue warps 12..15
 constexpr uint32_t TILE_BYTES = BM * BK * 4;  // 16 KB (A or B, raw or hi or lo)
 constexpr uint32_t RAW_BYTES = 2 * TILE_BYTES;
 constexpr uint32_t CONV_BYTES = 4 * TILE_BYTES;  // hiA loA hiB loB
-constexpr size_t SMEM = (size_t)RAW_STAGES * RAW_BYTES + (size_t)CONV_STAGES * CONV_BYTES + 1024 + 256;
+constexpr size_t SMEM = (size_t)RAW_STAGES * RAW_BYTES + (size_t)CONV_STAGES * CONV_BYTES + 1024 + 512;
 constexpr uint32_t TMEM_COLS = ACC_STAGES * BN;  // 256
 
 struct Args {
@@ -50,6 +50,7 @@ struct Args {
   float alpha, beta;
   float* C;
   long ldc;
+  int* sched;  // dynamic tile scheduler [ticket, done] (self-resetting) or null
 };
 
 // K-major, 128B-swizzled UMMA shared-memory descriptor (SM100, version 1):
@@ -139,7 +140,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(conv_empty + 8 * s, 1);
     }
     for (int s = 0; s < ACC_STAGES; ++s) {
-      mbar_init(acc_full + 8 * s, 1);
+      mbar_init(acc_full + 8 * s, 2);  // tcgen05.commit + the MMA lane's release arrive
       mbar_init(acc_empty + 8 * s, 4);
     }
     fence_barrier_init();
@@ -156,17 +157,44 @@ __global__ void __launch_bounds__(THREADS, 1)
   fence_after_sync();
   const uint32_t tmem_base = *tmem_slot;
 
+  // Tile ids (dynamic tickets, -1 = no more work) travel producer ->
+  // converters -> MMA -> epilogue through tq[], published before the first
+  // barrier arrival of each tile; the sentinel flows down the same barriers.
+  volatile int* tq = (volatile int*)(tmem_slot + 2);  // [16]
   if (warp == 0) {
     // ================= TMA producer =================
     if (lane == 0) {
       tma_prefetch_desc(&tmA);
       tma_prefetch_desc(&tmB);
       long g = 0;
-      for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+      int prev = -1;
+      for (int local = 0;; ++local) {
+        int tile;
+        if (!p.sched) {
+          tile = prev < 0 ? (int)blockIdx.x : prev + (int)gridDim.x;
+          if (tile >= p.tiles) tile = -1;
+        } else {
+          tile = atomicAdd(p.sched, 1);
+          if (tile >= p.tiles) {
+            tile = -1;
+            if (atomicAdd(p.sched + 1, 1) == (int)gridDim.x - 1) {
+              atomicExch(p.sched, 0);
+              atomicExch(p.sched + 1, 0);
+            }
+          }
+        }
+        prev = tile;
+        const int s0 = (int)(g % RAW_STAGES);
+        if (g >= RAW_STAGES) mbar_wait(raw_empty + 8 * s0, (uint32_t)(((g / RAW_STAGES) & 1) ^ 1));
+        tq[local & 15] = tile;
+        if (tile < 0) {
+          mbar_arrive(raw_full + 8 * s0);  // sentinel: completes the phase with no data
+          break;
+        }
         const int mc = (tile % p.tm) * BM, nc = (tile / p.tm) * BN;
         for (int kb = 0; kb < nk; ++kb, ++g) {
           const int s = (int)(g % RAW_STAGES);
-          if (g >= RAW_STAGES) mbar_wait(raw_empty + 8 * s, (uint32_t)(((g / RAW_STAGES) & 1) ^ 1));
+          if (kb > 0 && g >= RAW_STAGES) mbar_wait(raw_empty + 8 * s, (uint32_t)(((g / RAW_STAGES) & 1) ^ 1));
           const uint32_t fb = raw_full + 8 * s;
           mbar_arrive_expect_tx(fb, RAW_BYTES);
           const uint32_t dA = smem_u32(raw + s * RAW_BYTES), dB = dA + TILE_BYTES;
@@ -183,15 +211,25 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else if (warp == 1) {
     // ================= MMA issuer =================
     long g = 0;
-    int local = 0;
-    for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x, ++local) {
+    for (int local = 0;; ++local) {
       const int as = local % ACC_STAGES;
+      const int c0 = (int)(g % CONV_STAGES);
+      mbar_wait(conv_full + 8 * c0, (uint32_t)((g / CONV_STAGES) & 1));
+      const int tile = tq[local & 15];
       if (local >= ACC_STAGES) mbar_wait(acc_empty + 8 * as, (uint32_t)(((local / ACC_STAGES) & 1) ^ 1));
+      if (tile < 0) {
+        // sentinel to the epilogue: complete the accumulator phase (2 arrivals)
+        if (lane == 0) {
+          mbar_arrive(acc_full + 8 * as);
+          mbar_arrive(acc_full + 8 * as);
+        }
+        break;
+      }
       fence_after_sync();
       const uint32_t tmem_d = tmem_base + as * BN;
       for (int kb = 0; kb < nk; ++kb, ++g) {
         const int c = (int)(g % CONV_STAGES);
-        mbar_wait(conv_full + 8 * c, (uint32_t)((g / CONV_STAGES) & 1));
+        if (kb > 0) mbar_wait(conv_full + 8 * c, (uint32_t)((g / CONV_STAGES) & 1));
         fence_after_sync();
         if (lane == 0) {
           const uint32_t base = smem_u32(conv + c * CONV_BYTES);
@@ -206,7 +244,10 @@ __global__ void __launch_bounds__(THREADS, 1)
             umma_tf32(tmem_d, kmajor_sw128_desc(hiA + off), kmajor_sw128_desc(hiB + off), 1u);
           }
           umma_commit(conv_empty + 8 * c);
-          if (kb == nk - 1) umma_commit(acc_full + 8 * as);
+          if (kb == nk - 1) {
+            umma_commit(acc_full + 8 * as);
+            mbar_arrive(acc_full + 8 * as);  // release: publishes the tile id to the epilogue
+          }
         }
         __syncwarp();
       }
@@ -215,10 +256,23 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ================= converters: raw -> hi/lo, K-major SW128 =================
     const int ct = threadIdx.x - CONV_WARP0 * 32;  // 0..255
     long g = 0;
-    for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+    for (int local = 0;; ++local) {
+      {
+        const int s0 = (int)(g % RAW_STAGES);
+        mbar_wait(raw_full + 8 * s0, (uint32_t)((g / RAW_STAGES) & 1));
+      }
+      const int tile = tq[local & 15];
+      if (tile < 0) {
+        // sentinel to the MMA warp: complete the next conversion slot's phase
+        const int c = (int)(g % CONV_STAGES);
+        if (g >= CONV_STAGES) mbar_wait(conv_empty + 8 * c, (uint32_t)(((g / CONV_STAGES) & 1) ^ 1));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(conv_full + 8 * c);
+        break;
+      }
       for (int kb = 0; kb < nk; ++kb, ++g) {
         const int s = (int)(g % RAW_STAGES), c = (int)(g % CONV_STAGES);
-        mbar_wait(raw_full + 8 * s, (uint32_t)((g / RAW_STAGES) & 1));
+        if (kb > 0) mbar_wait(raw_full + 8 * s, (uint32_t)((g / RAW_STAGES) & 1));
         if (g >= CONV_STAGES) mbar_wait(conv_empty + 8 * c, (uint32_t)(((g / CONV_STAGES) & 1) ^ 1));
         const float* rA = (const float*)(raw + s * RAW_BYTES);
         const float* rB = rA + BM * BK;
@@ -266,11 +320,12 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else if (warp >= EPI_WARP0) {
     // ================= epilogue =================
     const int q = warp & 3;  // TMEM lane quarter
-    int local = 0;
-    for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x, ++local) {
+    for (int local = 0;; ++local) {
       const int as = local % ACC_STAGES;
-      const int mc = (tile % p.tm) * BM, nc = (tile / p.tm) * BN;
       mbar_wait(acc_full + 8 * as, (uint32_t)((local / ACC_STAGES) & 1));
+      const int tile = tq[local & 15];
+      if (tile < 0) break;
+      const int mc = (tile % p.tm) * BM, nc = (tile / p.tm) * BN;
       fence_after_sync();
       const int m = mc + q * 32 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
@@ -385,6 +440,7 @@ int sgemm_tf32x3(bool ta, bool tb, int M, int N, int K, float alpha, const float
   a.tiles = a.tm * a.tn;
   a.alpha = alpha; a.beta = beta;
   a.C = C; a.ldc = ldc;
+  a.sched = gemm_sched_slot(st);
   const int grid = a.tiles < num_sms() ? a.tiles : num_sms();
   ProfScope ps(PROF_GEMM_TF32, 2.0 * M * N * K,
                4.0 * ((double)M * K + (double)K * N + (beta != 0.0f ? 2.0 : 1.0) * M * N), st);

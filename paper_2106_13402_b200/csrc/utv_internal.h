@@ -37,6 +37,9 @@ constexpr size_t SPLITK_WS = 1024ull * 128 * 128;
 int choose_splits(int tiles, int K);
 // CTA budget for the next dgemm launches on this host thread (0 = all SMs).
 void gemm_set_max_ctas(int n);
+// Per-stream [ticket, done] counter pair of the dynamic tile schedulers
+// (self-resetting; kernels on one stream run in order, so they can share it).
+int* gemm_sched_slot(cudaStream_t st);
 size_t dgemm_ws_doubles(int M, int N, int K);
 int dgemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, long lda,
           const double* B, long ldb, double beta, double* C, long ldc, double* ws,
