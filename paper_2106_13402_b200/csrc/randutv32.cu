@@ -15,6 +15,8 @@
 //  * the compact-WY updates and the small-SVD rotations are 3xTF32 GEMMs.
 // Requirements: m, n, b multiples of 4 and leading dimensions multiples of 4
 // (TMA: 16-byte strides and sub-matrix origins).
+#include <mutex>
+
 #include "common.cuh"
 #include "utv_internal.h"
 
@@ -41,7 +43,7 @@ struct Ws32 {
   float *Y, *Z, *Yv, *Tv, *Yu, *Tu, *Us, *Vs, *W1, *W2, *tmp;
   long ldn, ldm, ldb, ldx;
   // fp64
-  double *P64, *Y64, *T64, *Us64, *Vs64, *sig, *red, *ss, *qr, *svd;
+  double *P64, *Y64, *T64, *Us64, *Vs64, *Rs, *sig, *red, *ss, *qr, *svd;
   long ld64;
   size_t qr_n, svd_n;
 };
@@ -78,6 +80,7 @@ size_t plan32(int m, int n, int b, Ws32* w, char* base) {
   v.T64 = (double*)take(8 * v.ldb * b);
   v.Us64 = (double*)take(8 * v.ldb * b);
   v.Vs64 = (double*)take(8 * v.ldb * b);
+  v.Rs = (double*)take(8 * v.ldb * b);
   v.sig = (double*)take(8 * v.ldb);
   v.red = (double*)take(8 * sumsq_scratch_doubles());
   v.ss = (double*)take(8 * 16);
@@ -146,8 +149,45 @@ int randutv_basic_f32(int m, int n, int b, int q, float* Tp, long ldt, float* Up
   plan32(m, n, b, &w, (char*)ws);
   F32Mat T{Tp, ldt, m, n}, U{Up, ldu, m, m}, V{Vp, ldv, n, n};
 
+  // Software-pipelined like the fp64 loop (randutv.cu): the fp64 Jacobi SVD
+  // of step i runs on a high-priority side stream (on a private copy of R)
+  // while the main stream runs step i's left transform and step i+1's
+  // sampling + Y-panel QR; step i's rotations follow on the main stream.
+  cudaStream_t s1 = nullptr;
+  cudaEvent_t ev[2];
+  {
+    static cudaStream_t g_s1 = nullptr;
+    static cudaEvent_t g_ev[2];
+    static std::once_flag once;
+    static int err = 0;
+    std::call_once(once, [] {
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      if (cudaStreamCreateWithPriority(&g_s1, cudaStreamNonBlocking, hi) != cudaSuccess) err = 1;
+      for (int e = 0; e < 2; ++e)
+        if (cudaEventCreateWithFlags(&g_ev[e], cudaEventDisableTiming) != cudaSuccess) err = 1;
+    });
+    if (err) return UTV_ERR_CUDA;
+    s1 = g_s1;
+    ev[0] = g_ev[0];
+    ev[1] = g_ev[1];
+  }
+  auto back = [&](int j) -> int {  // rotations, diag(sigma), error tracking of step j
+    const int lo = j * b, mid = lo + b, kc = n - lo;
+    UTV_CHECK(cvt_f64_to_f32(w.Us64, w.ldb, w.Us, w.ldb, b, b, st));
+    UTV_CHECK(cvt_f64_to_f32(w.Vs64, w.ldb, w.Vs, w.ldb, b, b, st));
+    UTV_CHECK(rot_right32(U.sub(0, lo, m, b), w.Us, w.ldb, b, w, st));
+    UTV_CHECK(rot_right32(V.sub(0, lo, n, b), w.Vs, w.ldb, b, w, st));
+    UTV_CHECK(set_diag_f32(T.at(lo, lo), T.ld, b, b, w.sig, st));
+    UTV_CHECK(rot_left_t32(T.sub(lo, mid, b, kc - b), w.Us, w.ldb, b, w, st));
+    UTV_CHECK(rot_right32(T.sub(0, lo, lo, b), w.Vs, w.ldb, b, w, st));
+    UTV_CHECK(sumsq_f32(T.at(lo, lo), T.ld, b, kc, errsq + j, w.red, st));
+    if (trail2) UTV_CHECK(sumsq_f32(T.at(mid, mid), T.ld, m - mid, kc - b, trail2 + j, w.red, st));
+    return UTV_OK;
+  };
   const int nsteps = (n + b - 1) / b;
   long gcol = 0;
+  int pending = -1;
   for (int i = 0; i < nsteps; ++i) {
     const int lo = i * b, mid = lo + b;
     const int k = m - lo, kc = n - lo;
@@ -164,29 +204,34 @@ int randutv_basic_f32(int m, int n, int b, int q, float* Tp, long ldt, float* Up
         UTV_CHECK(sgemm_tf32x3(true, false, kc, b, k, 1.0f, Bk.p, Bk.ld, w.Z, w.ldm, 0.0f, w.Y, w.ldn, st));
         UTV_CHECK(pow2_normalize_f32(w.Y, w.ldn, kc, b, w.ss, w.red, st));
       }
-      // ---- right transform (randutv.py:141-144) ----
       UTV_CHECK(panel_qr32(F32Mat{w.Y, w.ldn, kc, b}, w.Yv, w.ldn, w.Tv, w.ldb, w, st));
+      if (pending >= 0) {
+        UTV_CUDA(cudaStreamWaitEvent(st, ev[1], 0));
+        UTV_CHECK(back(pending));
+        pending = -1;
+      }
+      // ---- right transform (randutv.py:141-144) ----
       F32Mat Yv{w.Yv, w.ldn, kc, b}, Tv{w.Tv, w.ldb, b, b};
       UTV_CHECK(larfb32('R', false, Yv, Tv, T.sub(0, lo, m, kc), w, st));
       UTV_CHECK(larfb32('R', false, Yv, Tv, V.sub(0, lo, n, kc), w, st));
-      // ---- left transform (randutv.py:146-149) ----
+      // ---- left transform (randutv.py:146-149); R (fp64) kept for the SVD ----
       UTV_CHECK(panel_qr32(T.sub(lo, lo, k, b), w.Yu, w.ldm, w.Tu, w.ldb, w, st));
+      UTV_CHECK(copy_mat(w.P64, w.ld64, w.Rs, w.ldb, b, b, st));
+      UTV_CUDA(cudaEventRecord(ev[0], st));
+      UTV_CUDA(cudaStreamWaitEvent(s1, ev[0], 0));
+      UTV_CHECK(gesvj(Mat{w.Rs, w.ldb, b, b}, w.sig, Mat{w.Us64, w.ldb, b, b},
+                      Mat{w.Vs64, w.ldb, b, b}, w.svd, w.svd_n, svd_status + i, s1));
+      UTV_CUDA(cudaEventRecord(ev[1], s1));
+      pending = i;
       F32Mat Yu{w.Yu, w.ldm, k, b}, Tu{w.Tu, w.ldb, b, b};
       UTV_CHECK(larfb32('R', false, Yu, Tu, U.sub(0, lo, m, k), w, st));
       UTV_CHECK(larfb32('L', true, Yu, Tu, T.sub(lo, mid, k, kc - b), w, st));
-      // ---- b x b SVD (fp64 Jacobi on the fp64 R still in P64) + rotations ----
-      UTV_CHECK(gesvj(Mat{w.P64, w.ld64, b, b}, w.sig, Mat{w.Us64, w.ldb, b, b},
-                      Mat{w.Vs64, w.ldb, b, b}, w.svd, w.svd_n, svd_status + i, st));
-      UTV_CHECK(cvt_f64_to_f32(w.Us64, w.ldb, w.Us, w.ldb, b, b, st));
-      UTV_CHECK(cvt_f64_to_f32(w.Vs64, w.ldb, w.Vs, w.ldb, b, b, st));
-      UTV_CHECK(rot_right32(U.sub(0, lo, m, b), w.Us, w.ldb, b, w, st));
-      UTV_CHECK(rot_right32(V.sub(0, lo, n, b), w.Vs, w.ldb, b, w, st));
-      UTV_CHECK(set_diag_f32(T.at(lo, lo), T.ld, b, b, w.sig, st));
-      UTV_CHECK(rot_left_t32(T.sub(lo, mid, b, kc - b), w.Us, w.ldb, b, w, st));
-      UTV_CHECK(rot_right32(T.sub(0, lo, lo, b), w.Vs, w.ldb, b, w, st));
-      UTV_CHECK(sumsq_f32(T.at(lo, lo), T.ld, b, kc, errsq + i, w.red, st));
-      if (trail2) UTV_CHECK(sumsq_f32(T.at(mid, mid), T.ld, m - mid, kc - b, trail2 + i, w.red, st));
     } else {
+      if (pending >= 0) {
+        UTV_CUDA(cudaStreamWaitEvent(st, ev[1], 0));
+        UTV_CHECK(back(pending));
+        pending = -1;
+      }
       // ---- final narrow block (randutv.py:164-177) ----
       if (k > kc) {
         UTV_CHECK(panel_qr32(T.sub(lo, lo, k, kc), w.Yu, w.ldm, w.Tu, w.ldb, w, st));
@@ -205,7 +250,12 @@ int randutv_basic_f32(int m, int n, int b, int q, float* Tp, long ldt, float* Up
       UTV_CHECK(rot_right32(T.sub(0, lo, lo, kc), w.Vs, w.ldb, kc, w, st));
       UTV_CHECK(sumsq_f32(T.at(lo, lo), T.ld, k, kc, errsq + i, w.red, st));
       if (trail2) UTV_CUDA(cudaMemsetAsync(trail2 + i, 0, sizeof(double), st));
+      break;
     }
+  }
+  if (pending >= 0) {
+    UTV_CUDA(cudaStreamWaitEvent(st, ev[1], 0));
+    UTV_CHECK(back(pending));
   }
   return UTV_OK;
 }
