@@ -396,8 +396,9 @@ __global__ void __launch_bounds__(THREADS, 1) panel_qr_kernel(Args a) {
   }
 }
 
-inline void geometry(int rows, int* rc, int* G) {
-  int r = (rows + GMAX - 1) / GMAX;
+inline void geometry(int rows, int* rc, int* G, int max_ctas) {
+  const int gm = (max_ctas > 0 && max_ctas < GMAX) ? max_ctas : GMAX;
+  int r = (rows + gm - 1) / gm;
   r = (r + 31) / 32 * 32;
   if (r < RC_MIN) r = RC_MIN;
   *rc = r;
@@ -415,10 +416,11 @@ int panel_rows_max() { return pqr::RC_MAX * pqr::GMAX; }
 
 static bool g_panel_attr = false;
 
-int panel_qr(Mat P, Mat Y, Mat T, const double* fro2, double* ws, cudaStream_t st) {
+int panel_qr(Mat P, Mat Y, Mat T, const double* fro2, double* ws, cudaStream_t st, int max_ctas) {
   if (P.cols > pqr::PW || P.cols < 1 || P.rows < P.cols) return -1;
   int rc, G;
-  pqr::geometry(P.rows, &rc, &G);
+  pqr::geometry(P.rows, &rc, &G, max_ctas);
+  if (rc > pqr::RC_MAX) pqr::geometry(P.rows, &rc, &G, 0);  // too tall for the budget: all SMs
   if (rc > pqr::RC_MAX) {
     fprintf(stderr, "libutvb200: panel with %d rows exceeds the panel QR limit (%d)\n", P.rows,
             panel_rows_max());

@@ -101,6 +101,10 @@ static int merge_t(Mat Y, Mat T, int j0, int jb, double* S1, double* S2, double*
 
 // Right-looking blocked QR over QR_PANEL-wide panels (each one fused
 // panel_qr launch), K = 256 DMMA trailing updates, optional T merges.
+// Look-ahead: the trailing update of panel j is split into the next panel's
+// columns (narrow) and the rest (wide); panel j+1 is factored on a
+// high-priority side stream (on <= 32 SMs) while the wide update runs on the
+// others, taking the latency-bound panel off the critical path.
 static int geqrf_blocked(Mat P, Mat Y, Mat T, bool want_t, const double* fro2, Arena& ar,
                          cudaStream_t st) {
   const int rows = P.rows, cols = P.cols, blk = qr::PANEL;
@@ -111,15 +115,45 @@ static int geqrf_blocked(Mat P, Mat Y, Mat T, bool want_t, const double* fro2, A
   double* lfb = ar.take(lfb_n);
   if (!lfb) return UTV_ERR_WORKSPACE;
   double* gws = lfb + (lfb_n - SPLITK_WS);
+  cudaStream_t sa = nullptr;
+  cudaEvent_t ev_narrow = nullptr, ev_panel = nullptr;
+  const bool lookahead = cols > blk;
+  if (lookahead) {
+    UTV_CHECK(aux_stream(1, &sa));
+    UTV_CHECK(aux_event(4, &ev_narrow));
+    UTV_CHECK(aux_event(5, &ev_panel));
+  }
+  constexpr int LA_CTAS = 32;
+  bool factored = false;  // panel j0 already factored (look-ahead) on sa
   for (int j0 = 0; j0 < cols; j0 += blk) {
     const int jb = cols - j0 < blk ? cols - j0 : blk;
-    Mat Pp = P.sub(j0, j0, rows - j0, jb);
     Mat Yp = Y.sub(j0, j0, rows - j0, jb);
     Mat Tp = T.sub(j0, j0, jb, jb);
-    if (j0 > 0) UTV_CHECK(set_zero(Y.at(0, j0), Y.ld, j0, jb, st));
-    UTV_CHECK(panel_qr(Pp, Yp, Tp, fro2, pws, st));
-    if (j0 + jb < cols)
-      UTV_CHECK(larfb('L', true, Yp, Tp, P.sub(j0, j0 + jb, rows - j0, cols - j0 - jb), lfb, lfb_n, st));
+    if (factored) {
+      UTV_CUDA(cudaStreamWaitEvent(st, ev_panel, 0));
+    } else {
+      if (j0 > 0) UTV_CHECK(set_zero(Y.at(0, j0), Y.ld, j0, jb, st));
+      UTV_CHECK(panel_qr(P.sub(j0, j0, rows - j0, jb), Yp, Tp, fro2, pws, st));
+    }
+    factored = false;
+    const int j1 = j0 + jb;
+    if (j1 < cols) {
+      const int jb1 = cols - j1 < blk ? cols - j1 : blk;
+      Mat Bn = P.sub(j0, j1, rows - j0, jb1);
+      UTV_CHECK(larfb('L', true, Yp, Tp, Bn, lfb, lfb_n, st));
+      if (j1 + jb1 < cols) {
+        // panel j+1 on the side stream, the wide update on the main stream
+        UTV_CUDA(cudaEventRecord(ev_narrow, st));
+        UTV_CUDA(cudaStreamWaitEvent(sa, ev_narrow, 0));
+        UTV_CHECK(set_zero(Y.at(0, j1), Y.ld, j1, jb1, sa));
+        UTV_CHECK(panel_qr(P.sub(j1, j1, rows - j1, jb1), Y.sub(j1, j1, rows - j1, jb1),
+                           T.sub(j1, j1, jb1, jb1), fro2, pws, sa, LA_CTAS));
+        UTV_CUDA(cudaEventRecord(ev_panel, sa));
+        factored = true;
+        UTV_CHECK(larfb('L', true, Yp, Tp, P.sub(j0, j1 + jb1, rows - j0, cols - j1 - jb1), lfb,
+                        lfb_n, st));
+      }
+    }
     if (want_t) UTV_CHECK(merge_t(Y, T, j0, jb, S1, S2, gws, st));
   }
   return UTV_OK;

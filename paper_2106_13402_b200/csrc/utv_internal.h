@@ -10,6 +10,12 @@ namespace utv {
 
 int num_sms();
 
+// ---- auxiliary streams / events (streams.cu) ----
+// stream 0: randUTV side-stream SVD; stream 1: blocked-QR look-ahead panels.
+// events 0-1: randUTV fp64, 2-3: randUTV fp32, 4-5: QR look-ahead.
+int aux_stream(int idx, cudaStream_t* s);
+int aux_event(int idx, cudaEvent_t* e);
+
 // ---- launch accounting / profiling (prof.cu) ----
 enum ProfCat {
   PROF_GEMM = 0,      // DMMA GEMM kernel (flops = 2MNK)
@@ -87,7 +93,8 @@ size_t geqrf_ws_doubles(int rows, int cols, bool want_t);
 // P <- R, Y, T (full cols x cols forward triangle; T must be zero below the diagonal).
 size_t panel_ws_doubles();
 int panel_rows_max();
-int panel_qr(Mat P, Mat Y, Mat T, const double* fro2, double* ws, cudaStream_t st);
+int panel_qr(Mat P, Mat Y, Mat T, const double* fro2, double* ws, cudaStream_t st,
+             int max_ctas = 0);
 int geqrf(Mat P, Mat Y, Mat Tw, bool want_t, double* ws, size_t ws_doubles, cudaStream_t st);
 
 // ---- K2 compact-WY apply (qr.cu) ----
