@@ -15,6 +15,8 @@
 //    intra-panel updates and larft fused, slab-resident leaves);
 //  * panels are combined right-looking with K=256 DMMA GEMM updates;
 //    triangles merge as T12 = -T1 (Y1^T Y2) T2.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "utv_internal.h"
 
@@ -103,7 +105,7 @@ static int merge_t(Mat Y, Mat T, int j0, int jb, double* S1, double* S2, double*
 // panel_qr launch), K = 256 DMMA trailing updates, optional T merges.
 // Look-ahead: the trailing update of panel j is split into the next panel's
 // columns (narrow) and the rest (wide); panel j+1 is factored on a
-// high-priority side stream (on <= 32 SMs) while the wide update runs on the
+// high-priority side stream (on <= 48 SMs) while the wide update runs on the
 // others, taking the latency-bound panel off the critical path.
 static int geqrf_blocked(Mat P, Mat Y, Mat T, bool want_t, const double* fro2, Arena& ar,
                          cudaStream_t st) {
@@ -123,7 +125,11 @@ static int geqrf_blocked(Mat P, Mat Y, Mat T, bool want_t, const double* fro2, A
     UTV_CHECK(aux_event(4, &ev_narrow));
     UTV_CHECK(aux_event(5, &ev_panel));
   }
-  constexpr int LA_CTAS = 32;
+  static const int LA_CTAS = [] {
+    const char* e = getenv("UTV_LA_CTAS");  // tuning knob (default 48)
+    const int v = e ? atoi(e) : 0;
+    return v > 0 ? v : 48;
+  }();
   bool factored = false;  // panel j0 already factored (look-ahead) on sa
   for (int j0 = 0; j0 < cols; j0 += blk) {
     const int jb = cols - j0 < blk ? cols - j0 : blk;
