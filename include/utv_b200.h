@@ -87,6 +87,10 @@ int utv_dlaset(char uplo, int m, int n, double alpha, double beta, double* A, lo
                void* stream);
 int utv_ddiag_scale(char side, int m, int n, const double* d, double alpha, double* A, long lda,
                     void* stream);
+/* B (n x m) = A^T (A is m x n).  Used to take a C-order host draw (the
+ * reference's gaussian() before its np.asfortranarray copy, matrix.py:52-60)
+ * to column-major on the device instead of transposing 2 GiB on the host. */
+int utv_dtranspose(int m, int n, const double* A, long lda, double* B, long ldb, void* stream);
 /* Zero the strictly upper ('U') or strictly lower ('L') part of A (diagonal kept). */
 int utv_dtri_zero(char uplo, int m, int n, double* A, long lda, void* stream);
 
@@ -133,6 +137,14 @@ int utv_randutv_basic_f64(int m, int n, int b, int q, double* T, long ldt, doubl
                           double* V, long ldv, const double* G, long ldg, double* errsq,
                           double* trail2, int* svd_status, void* work, size_t lwork,
                           void* stream);
+
+/* Steps [i0, i1) of utv_randutv_basic_f64 (same workspace; G = the block of
+ * step i0 at column 0).  Lets the host draw later steps' Gaussian blocks
+ * while earlier steps run; consecutive ranges give the same bits as one call. */
+int utv_randutv_basic_steps_f64(int i0, int i1, int m, int n, int b, int q, double* T, long ldt,
+                                double* U, long ldu, double* V, long ldv, const double* G, long ldg,
+                                double* errsq, double* trail2, int* svd_status, void* work,
+                                size_t lwork, void* stream);
 
 /* One step i (0-based) of blocked randUTV — the host loop of the boosted
  * (Algorithm 2) and partial variants (randutv_boosted / randutv_partial,

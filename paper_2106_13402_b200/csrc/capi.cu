@@ -10,6 +10,9 @@ int randutv_basic(int m, int n, int b, int q, Mat T, Mat U, Mat V, const double*
                   double* errsq, double* trail2, int* svd_status, double* ws, size_t ws_doubles,
                   cudaStream_t st);
 size_t randutv_ws_doubles_p(int m, int n, int b, int p);
+int randutv_basic_range(int i0, int i1, int m, int n, int b, int q, Mat T, Mat U, Mat V,
+                        const double* G, long ldg, double* errsq, double* trail2, int* svd_status,
+                        double* ws, size_t ws_doubles, cudaStream_t st);
 int randutv_step(int i, int m, int n, int b, int p, int q, bool boosted, Mat T, Mat U, Mat V,
                  const double* G, long ldg, double* errsq, double* trail2, int* svd_status,
                  double* ws, size_t ws_doubles, int* carried, int* is_final, cudaStream_t st);
@@ -107,6 +110,22 @@ int utv_dlarfb(char side, char trans, int m, int n, int k, int w, const double* 
 
 int utv_dgeqrf_rows_max(void) { return panel_rows_max(); }
 
+int utv_randutv_basic_steps_f64(int i0, int i1, int m, int n, int b, int q, double* T, long ldt,
+                                double* U, long ldu, double* V, long ldv, const double* G, long ldg,
+                                double* errsq, double* trail2, int* svd_status, void* work,
+                                size_t lwork, void* stream) {
+  if (i0 < 0 || i1 < i0) return -1;
+  if (m < n || n < 1) return -3;
+  if (b < 1 || b > 1024) return -5;
+  if (q < 0) return -6;
+  if (!ld_ok(ldt, m)) return -8;
+  if (!ld_ok(ldu, m)) return -10;
+  if (!ld_ok(ldv, n)) return -12;
+  return randutv_basic_range(i0, i1, m, n, b, q, Mat{T, ldt, m, n}, Mat{U, ldu, m, m},
+                             Mat{V, ldv, n, n}, G, ldg, errsq, trail2, svd_status, (double*)work,
+                             lwork / sizeof(double), S(stream));
+}
+
 size_t utv_randutv_step_bufsize(int m, int n, int b, int p, int) { return B(randutv_ws_doubles_p(m, n, b, p)); }
 
 int utv_randutv_step_f64(int i, int m, int n, int b, int p, int q, int boosted, double* T, long ldt,
@@ -176,6 +195,14 @@ int utv_dlaset(char uplo, int m, int n, double alpha, double beta, double* A, lo
   if (n < 0) return -3;
   if (lda < m) return -7;
   return laset(u, m, n, alpha, beta, A, lda, S(stream));
+}
+
+int utv_dtranspose(int m, int n, const double* A, long lda, double* Bm, long ldb, void* stream) {
+  if (m < 0) return -1;
+  if (n < 0) return -2;
+  if (lda < m) return -4;
+  if (ldb < n) return -6;
+  return transpose(A, lda, Bm, ldb, m, n, S(stream));
 }
 
 int utv_dtri_zero(char uplo, int m, int n, double* A, long lda, void* stream) {

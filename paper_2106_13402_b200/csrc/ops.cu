@@ -168,6 +168,22 @@ __global__ void diag_f32_kernel(float* A, long lda, int rows, int cols, const do
   }
 }
 
+// B (n x m) = A^T (A m x n), 32 x 32 tiles through padded shared memory.
+__global__ void transpose_kernel(const double* __restrict__ A, long lda, double* __restrict__ B,
+                                 long ldb, int m, int n) {
+  __shared__ double tile[32][33];
+  const int r0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int r = r0 + threadIdx.x, c = c0 + j;
+    if (r < m && c < n) tile[j][threadIdx.x] = A[r + (long)c * lda];
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int r = c0 + threadIdx.x, c = r0 + j;  // B row = A col
+    if (r < n && c < m) B[r + (long)c * ldb] = tile[threadIdx.x][j];
+  }
+}
+
 inline int grid_for(long total) {
   const long g = (total + 255) / 256;
   const long cap = 8L * num_sms();
@@ -291,6 +307,15 @@ int set_diag_f32(float* A, long lda, int nr, int nc, const double* d, cudaStream
   if (nr <= 0 || nc <= 0) return UTV_OK;
   ProfScope ps(PROF_OPS, 0.0, 4.0 * nr * nc, st);
   ops::diag_f32_kernel<<<ops::grid_for((long)nr * nc), 256, 0, st>>>(A, lda, nr, nc, d);
+  UTV_CUDA(cudaGetLastError());
+  return UTV_OK;
+}
+
+int transpose(const double* A, long lda, double* B, long ldb, int m, int n, cudaStream_t st) {
+  if (m <= 0 || n <= 0) return UTV_OK;
+  ProfScope ps(PROF_OPS, 0.0, 16.0 * m * n, st);
+  dim3 grid(ceil_div(m, 32), ceil_div(n, 32)), block(32, 8);
+  ops::transpose_kernel<<<grid, block, 0, st>>>(A, lda, B, ldb, m, n);
   UTV_CUDA(cudaGetLastError());
   return UTV_OK;
 }

@@ -289,9 +289,22 @@ static int side_stream(cudaStream_t* s1, cudaEvent_t* ev) {
 // right transform (the first operation that touches rows lo:mid of T
 // again).  Data dependencies are unchanged, so results are bitwise the same
 // as the one-stream step sequence.
+int randutv_basic_range(int i0, int i1, int m, int n, int b, int q, Mat T, Mat U, Mat V,
+                        const double* G, long ldg, double* errsq, double* trail2, int* svd_status,
+                        double* ws, size_t ws_doubles, cudaStream_t st);
+
 int randutv_basic(int m, int n, int b, int q, Mat T, Mat U, Mat V, const double* G, long ldg,
                   double* errsq, double* trail2, int* svd_status, double* ws, size_t ws_doubles,
                   cudaStream_t st) {
+  return randutv_basic_range(0, (n + b - 1) / b, m, n, b, q, T, U, V, G, ldg, errsq, trail2,
+                             svd_status, ws, ws_doubles, st);
+}
+
+// Steps [i0, i1) of the basic loop (G = the block of step i0 at column 0).
+// Lets the host draw the next steps' Gaussian blocks while these run.
+int randutv_basic_range(int i0, int i1, int m, int n, int b, int q, Mat T, Mat U, Mat V,
+                        const double* G, long ldg, double* errsq, double* trail2, int* svd_status,
+                        double* ws, size_t ws_doubles, cudaStream_t st) {
   if (m < n) return -1;
   if (b < 1) return -3;
   if (q < 0) return -4;
@@ -301,10 +314,10 @@ int randutv_basic(int m, int n, int b, int q, Mat T, Mat U, Mat V, const double*
   cudaStream_t s1;
   cudaEvent_t ev[2];  // [0] R ready (main), [1] SVD done (side)
   UTV_CHECK(side_stream(&s1, ev));
-  const int nsteps = (n + b - 1) / b;
+  const int nsteps = (n + b - 1) / b < i1 ? (n + b - 1) / b : i1;
   long gcol = 0;
   int pending = -1;  // step whose SVD is in flight on the side stream
-  for (int i = 0; i < nsteps; ++i) {
+  for (int i = i0; i < nsteps; ++i) {
     const int lo = i * b;
     const int k = m - lo, kc = n - lo;
     if (kc <= b) {

@@ -70,6 +70,8 @@ int laset(int uplo, int rows, int cols, double alpha, double beta, double* A, lo
 // A <- alpha diag(d) A (side 0) or alpha A diag(d) (side 1).
 int diag_scale(int side, int rows, int cols, const double* d, double alpha, double* A, long lda,
                cudaStream_t st);
+// B (n x m) = A^T (A m x n)
+int transpose(const double* A, long lda, double* B, long ldb, int m, int n, cudaStream_t st);
 // fp32 helpers of the C5 path (ops.cu)
 int sumsq_f32(const float* A, long lda, int rows, int cols, double* out, double* scratch,
               cudaStream_t st);

@@ -216,6 +216,26 @@ def laset(uplo, alpha, beta, A: DMat):
     return A
 
 
+def transpose(A: DMat, B: DMat | None = None):
+    """B = A^T on the device."""
+    if B is None:
+        B = dempty(A.cols, A.rows)
+    check(load().utv_dtranspose(A.rows, A.cols, A.ptr, A.ld, B.ptr, B.ld, stream_ptr()),
+          "utv_dtranspose")
+    return B
+
+
+def from_numpy_any_order(a):
+    """Device copy of a 2-D float64 array without a host-side layout copy:
+    F-order arrays go up as is; C-order arrays go up as their transpose
+    (the same bytes) and are transposed on the device."""
+    from ._lib import dfrom_numpy
+    a = np.asarray(a, dtype=np.float64)
+    if a.flags["F_CONTIGUOUS"] or not a.flags["C_CONTIGUOUS"]:
+        return dfrom_numpy(a)
+    return transpose(dfrom_numpy(a.T))
+
+
 def tri_zero(uplo, A: DMat):
     """Zero the strictly upper ('U') or strictly lower ('L') part; diagonal kept."""
     check(load().utv_dtri_zero(uplo.encode(), A.rows, A.cols, A.ptr, A.ld, stream_ptr()),

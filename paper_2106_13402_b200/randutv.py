@@ -146,6 +146,8 @@ def randutv_basic(a, b, q, rng, record_trailing=False, *, dtype=np.float64):
     f32 = np.dtype(dtype) == np.float32
     if f32 and (m % 4 or n % 4 or b % 4):
         raise ValueError("the fp32 variant needs m, n and b to be multiples of 4")
+    if not f32:
+        return _randutv_basic_pipelined(a, b, q, rng, record_trailing)
     blocks = draw_sample_blocks(rng, m, n, b)
     if f32:
         t_dev = dfrom_numpy(a, dtype=torch.float32)
@@ -155,6 +157,10 @@ def randutv_basic(a, b, q, rng, record_trailing=False, *, dtype=np.float64):
         t_dev = dfrom_numpy(a)
         g_dev = dv.stage_randutv_blocks(blocks, b)
         run, U, V = randutv_basic_device(t_dev, b, q, g_dev, record_trailing)
+    return _finish_basic(a, b, q, run, t_dev, U, V, record_trailing, f32)
+
+
+def _finish_basic(a, b, q, run, t_dev, U, V, record_trailing, f32):
     status = run.status.cpu().numpy()
     if (status < 0).any():
         raise ConvergenceError("b x b Jacobi SVD failed to converge")
@@ -234,6 +240,80 @@ def _randutv_stepwise(a, b, q, p, rng, boosted, tol_fro=None, max_rank=None,
         U=np.asfortranarray(U.to_numpy()), T=np.asfortranarray(t_dev.to_numpy()),
         V=np.asfortranarray(V.to_numpy()), b=b, steps_done=steps, oversample=p, power=q,
         errors=list(tracker.history), trailing_fro=trailing)
+
+
+_GRING = {}
+
+
+def _pinned_pair(nbytes):
+    """Two cached pinned host buffers of >= nbytes (the G-block staging ring)."""
+    import torch
+    key = 1 << max(20, (int(nbytes) - 1).bit_length())
+    if key not in _GRING:
+        _GRING.clear()
+        _GRING[key] = [(torch.empty(key // 8, dtype=torch.float64, pin_memory=True), torch.cuda.Event())
+                       for _ in range(2)]
+    return _GRING[key]
+
+
+def _draw_into(rng, k, b, out):
+    """rng.standard_normal(k, b) written into out (same draws as the reference)."""
+    gen = getattr(rng, "_gen", None)
+    if gen is not None:
+        gen.standard_normal((k, b), out=out)
+    else:
+        out[...] = rng.standard_normal(k, b)
+
+
+def _randutv_basic_pipelined(a, b, q, rng, record_trailing):
+    """fp64 randutv_basic with the host RNG overlapped with the device loop:
+    the Gaussian blocks of the next group of steps are drawn straight into a
+    pinned buffer and copied up on a side stream while the current group
+    runs (utv_randutv_basic_steps_f64); draw order and values are exactly the
+    reference's (randutv.py:189)."""
+    import torch
+
+    from . import _lib
+    m, n = a.shape
+    lib = _lib.load()
+    steps = -(-n // b)
+    sizes = [m - i * b for i in range(max(0, steps - 1))]       # rows of each drawn block
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64) if sizes else np.zeros(1, np.int64)
+    t_dev = dfrom_numpy(a)
+    run = dv.RandUtvRun(m, n, b, q, record_trailing)
+    U, V = deye(m), deye(n)
+    G = _lib.dempty(b, max(int(offs[-1]), 1))               # block i = columns offs[i]:offs[i+1]
+    groups, i = [], 0
+    for width in [1, 3] + [4] * steps:                      # small first group: start the GPU early
+        if i >= steps:
+            break
+        groups.append((i, min(steps, i + width)))
+        i += width
+    maxcols = max((offs[min(j1, len(sizes))] - offs[j0] for j0, j1 in groups), default=1)
+    ring = _pinned_pair(8 * b * max(int(maxcols), 1))
+    copy_stream = torch.cuda.Stream()
+    comp = torch.cuda.current_stream()
+    for gi, (j0, j1) in enumerate(groups):
+        d0, d1 = min(j0, len(sizes)), min(j1, len(sizes))
+        ncol = int(offs[d1] - offs[d0])
+        if ncol > 0:
+            buf, ev = ring[gi % 2]
+            ev.synchronize()                                  # previous upload from this buffer done
+            host = buf.numpy()
+            for j in range(d0, d1):
+                lo, hi = int(offs[j] - offs[d0]) * b, int(offs[j + 1] - offs[d0]) * b
+                _draw_into(rng, sizes[j], b, host[lo:hi].reshape(sizes[j], b))
+            with torch.cuda.stream(copy_stream):
+                G.t[int(offs[d0]):int(offs[d1]), :b].copy_(buf[: ncol * b].view(ncol, b), non_blocking=True)
+                ev.record(copy_stream)
+            comp.wait_event(ev)
+        gptr = G.at(0, int(offs[d0])) if ncol > 0 else G.ptr
+        _lib.check(lib.utv_randutv_basic_steps_f64(
+            j0, j1, m, n, b, q, t_dev.ptr, t_dev.ld, U.ptr, U.ld, V.ptr, V.ld, gptr, G.ld,
+            run.errsq.data_ptr(), run.trail2.data_ptr() if run.trail2 is not None else None,
+            run.status.data_ptr(), run.ws.data_ptr(), run.lw, _lib.stream_ptr()),
+            "utv_randutv_basic_steps_f64")
+    return _finish_basic(a, b, q, run, t_dev, U, V, record_trailing, False)
 
 
 def randutv_boosted(a, b, q, p, rng, record_trailing=False):
