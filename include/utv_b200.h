@@ -79,6 +79,15 @@ int utv_dlarfb(char side, char trans, int m, int n, int k, int w, const double* 
  * inputs are split into row chunks by the caller (TSQR). */
 int utv_dgeqrf_rows_max(void);
 
+/* Device generators (matgen.py:58-91: gen_bie, gen_kahan) and the Frobenius
+ * error curve e_k = ||T[k:, k:]||_F, k = 1..n-1 (bench.py:63-72) -> e (device,
+ * n-1 doubles), O(mn), fixed-order (bitwise reproducible). */
+int utv_dgen_bie(int n, double* A, long lda, void* stream);
+int utv_dgen_kahan(int n, double theta, double* A, long lda, void* stream);
+size_t utv_dtrailing_fro_bufsize(int m, int n);
+int utv_dtrailing_fro(int m, int n, const double* T, long ldt, double* e, void* work, size_t lwork,
+                      void* stream);
+
 /* Block utilities for the TSQR tree (LAPACK dlacpy / dlaset semantics):
  * B <- A;  A <- alpha off the diagonal of the uplo ('U', 'L', 'A') part, beta
  * on the diagonal;  A <- alpha diag(d) A (side 'L') or alpha A diag(d) ('R'). */

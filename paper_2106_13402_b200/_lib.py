@@ -70,6 +70,11 @@ SIGNATURES = {
     "utv_dlaset": (c_int, [c_char, c_int, c_int, c_double, c_double, c_void_p, c_long, c_void_p]),
     "utv_dtri_zero": (c_int, [c_char, c_int, c_int, c_void_p, c_long, c_void_p]),
     "utv_dtranspose": (c_int, [c_int, c_int, c_void_p, c_long, c_void_p, c_long, c_void_p]),
+    "utv_dgen_bie": (c_int, [c_int, c_void_p, c_long, c_void_p]),
+    "utv_dgen_kahan": (c_int, [c_int, c_double, c_void_p, c_long, c_void_p]),
+    "utv_dtrailing_fro_bufsize": (c_size_t, [c_int, c_int]),
+    "utv_dtrailing_fro": (c_int, [c_int, c_int, c_void_p, c_long, c_void_p, c_void_p, c_size_t,
+                                  c_void_p]),
     "utv_ddiag_scale": (c_int, [c_char, c_int, c_int, c_void_p, c_double, c_void_p, c_long,
                                 c_void_p]),
     "utv_dgetrf_signed_bufsize": (c_size_t, [c_int, c_int]),

@@ -205,6 +205,29 @@ int utv_dtranspose(int m, int n, const double* A, long lda, double* Bm, long ldb
   return transpose(A, lda, Bm, ldb, m, n, S(stream));
 }
 
+int utv_dgen_bie(int n, double* A, long lda, void* stream) {
+  if (n < 1) return -1;
+  if (lda < n) return -3;
+  return gen_bie(A, lda, n, S(stream));
+}
+
+int utv_dgen_kahan(int n, double theta, double* A, long lda, void* stream) {
+  if (n < 1) return -1;
+  if (lda < n) return -4;
+  return gen_kahan(A, lda, n, theta, S(stream));
+}
+
+size_t utv_dtrailing_fro_bufsize(int m, int n) { return B(trailing_fro_ws_doubles(m, n)); }
+
+int utv_dtrailing_fro(int m, int n, const double* T, long ldt, double* e, void* work, size_t lwork,
+                      void* stream) {
+  if (m < 1) return -1;
+  if (n < 1) return -2;
+  if (ldt < m) return -4;
+  if (lwork < trailing_fro_ws_doubles(m, n) * sizeof(double)) return UTV_ERR_WORKSPACE;
+  return trailing_fro(T, ldt, m, n, e, (double*)work, S(stream));
+}
+
 int utv_dtri_zero(char uplo, int m, int n, double* A, long lda, void* stream) {
   int u;
   if (uplo == 'U' || uplo == 'u') u = 3;

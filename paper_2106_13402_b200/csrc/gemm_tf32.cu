@@ -20,9 +20,12 @@
 //               the canonical K-major 128B-swizzled UMMA layout (also turns
 //               MN-major operands K-major, so one descriptor form serves all
 //               four op combinations); fence.proxy.async before arrival
-//   warps 12-15 epilogue: tcgen05.ld 32x32b from a double-buffered TMEM
-//               accumulator (2 x 128 columns), alpha/beta, coalesced stores;
-//               overlaps the next tile's MMAs.
+//   warps 12-27 epilogue: tcgen05.ld 32x32b from a double-buffered TMEM
+//               accumulator (2 x 128 columns).  The tensor-core FP32
+//               accumulator does not round to nearest, so K is split into
+//               512-deep chunks whose partial tiles are summed in registers
+//               (RN) — long-K products stay fp32-accurate; alpha/beta,
+//               coalesced stores; overlaps the next tile's MMAs.
 #include <cudaTypedefs.h>
 
 #include <mutex>
@@ -35,9 +38,11 @@ namespace utv {
 namespace tf32 {
 constexpr int BM = 128, BN = 128, BK = 32;
 constexpr int RAW_STAGES = 2, CONV_STAGES = 2, ACC_STAGES = 2;
-constexpr int THREADS = 512;                  // 16 warps
+constexpr int THREADS = 896;                  // 28 warps
 constexpr int CONV_WARP0 = 4, NCONV = 8;      // converter warps 4..11
-constexpr int EPI_WARP0 = 12;                 // epilogue warps 12..15
+constexpr int EPI_WARP0 = 12;                 // epilogue warps 12..27 (4 per TMEM lane quarter)
+constexpr int EPI_COLS = 32;                  // accumulator columns per epilogue thread
+constexpr int CHUNK_KB = 16;                  // k-blocks (512 k) per TMEM accumulation chunk
 constexpr uint32_t TILE_BYTES = BM * BK * 4;  // 16 KB (A or B, raw or hi or lo)
 constexpr uint32_t RAW_BYTES = 2 * TILE_BYTES;
 constexpr uint32_t CONV_BYTES = 4 * TILE_BYTES;  // hiA loA hiB loB
@@ -141,7 +146,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int s = 0; s < ACC_STAGES; ++s) {
       mbar_init(acc_full + 8 * s, 2);  // tcgen05.commit + the MMA lane's release arrive
-      mbar_init(acc_empty + 8 * s, 4);
+      mbar_init(acc_empty + 8 * s, 16);
     }
     fence_barrier_init();
   }
@@ -210,46 +215,55 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else if (warp == 1) {
     // ================= MMA issuer =================
+    // The tensor-core FP32 accumulator does not round to nearest, so long K
+    // sums drift; every CHUNK_KB k-blocks the accumulator goes to the
+    // epilogue, which adds the chunks in registers (RN).  Chunks alternate
+    // between the two TMEM buffers.
     long g = 0;
+    long ch = 0;  // global chunk counter (TMEM buffer = ch % ACC_STAGES)
     for (int local = 0;; ++local) {
-      const int as = local % ACC_STAGES;
       const int c0 = (int)(g % CONV_STAGES);
       mbar_wait(conv_full + 8 * c0, (uint32_t)((g / CONV_STAGES) & 1));
       const int tile = tq[local & 15];
-      if (local >= ACC_STAGES) mbar_wait(acc_empty + 8 * as, (uint32_t)(((local / ACC_STAGES) & 1) ^ 1));
       if (tile < 0) {
-        // sentinel to the epilogue: complete the accumulator phase (2 arrivals)
-        if (lane == 0) {
+        const int as = (int)(ch % ACC_STAGES);
+        if (ch >= ACC_STAGES) mbar_wait(acc_empty + 8 * as, (uint32_t)(((ch / ACC_STAGES) & 1) ^ 1));
+        if (lane == 0) {  // sentinel to the epilogue (2 arrivals complete the phase)
           mbar_arrive(acc_full + 8 * as);
           mbar_arrive(acc_full + 8 * as);
         }
         break;
       }
-      fence_after_sync();
-      const uint32_t tmem_d = tmem_base + as * BN;
       for (int kb = 0; kb < nk; ++kb, ++g) {
+        const int as = (int)(ch % ACC_STAGES);
+        const bool chunk_start = (kb % CHUNK_KB) == 0;
+        const bool chunk_end = (kb % CHUNK_KB) == CHUNK_KB - 1 || kb == nk - 1;
+        if (chunk_start && ch >= ACC_STAGES)
+          mbar_wait(acc_empty + 8 * as, (uint32_t)(((ch / ACC_STAGES) & 1) ^ 1));
         const int c = (int)(g % CONV_STAGES);
         if (kb > 0) mbar_wait(conv_full + 8 * c, (uint32_t)((g / CONV_STAGES) & 1));
         fence_after_sync();
         if (lane == 0) {
+          const uint32_t tmem_d = tmem_base + as * BN;
           const uint32_t base = smem_u32(conv + c * CONV_BYTES);
           const uint32_t hiA = base, loA = base + TILE_BYTES, hiB = base + 2 * TILE_BYTES,
                          loB = base + 3 * TILE_BYTES;
 #pragma unroll
           for (int ks = 0; ks < BK / 8; ++ks) {
             const uint32_t off = ks * 32;  // 8 tf32 = 32 bytes along K
-            const uint32_t acc0 = (kb > 0 || ks > 0) ? 1u : 0u;
+            const uint32_t acc0 = (!chunk_start || ks > 0) ? 1u : 0u;
             umma_tf32(tmem_d, kmajor_sw128_desc(loA + off), kmajor_sw128_desc(hiB + off), acc0);
             umma_tf32(tmem_d, kmajor_sw128_desc(hiA + off), kmajor_sw128_desc(loB + off), 1u);
             umma_tf32(tmem_d, kmajor_sw128_desc(hiA + off), kmajor_sw128_desc(hiB + off), 1u);
           }
           umma_commit(conv_empty + 8 * c);
-          if (kb == nk - 1) {
+          if (chunk_end) {
             umma_commit(acc_full + 8 * as);
             mbar_arrive(acc_full + 8 * as);  // release: publishes the tile id to the epilogue
           }
         }
         __syncwarp();
+        if (chunk_end) ++ch;
       }
     }
   } else if (warp >= CONV_WARP0 && warp < CONV_WARP0 + NCONV) {
@@ -319,21 +333,42 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else if (warp >= EPI_WARP0) {
     // ================= epilogue =================
-    const int q = warp & 3;  // TMEM lane quarter
+    // 16 warps: lane quarter q = warp & 3 (TMEM lanes 32q..32q+31), column
+    // slice h = (warp - EPI_WARP0) >> 2 (EPI_COLS columns).  Chunk
+    // accumulators are summed in registers with round-to-nearest adds, then
+    // written once per tile.
+    const int q = warp & 3, h = (warp - EPI_WARP0) >> 2;
+    const int nchunk = (nk + CHUNK_KB - 1) / CHUNK_KB;
+    long ch = 0;
     for (int local = 0;; ++local) {
-      const int as = local % ACC_STAGES;
-      mbar_wait(acc_full + 8 * as, (uint32_t)((local / ACC_STAGES) & 1));
-      const int tile = tq[local & 15];
+      float acc[EPI_COLS];
+      int tile = 0;
+      for (int cc = 0; cc < nchunk; ++cc, ++ch) {
+        const int as = (int)(ch % ACC_STAGES);
+        mbar_wait(acc_full + 8 * as, (uint32_t)((ch / ACC_STAGES) & 1));
+        if (cc == 0) {
+          tile = tq[local & 15];
+          if (tile < 0) break;
+        }
+        fence_after_sync();
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + h * EPI_COLS;
+#pragma unroll
+        for (int c0 = 0; c0 < EPI_COLS; c0 += 16) {
+          float v[16];
+          tmem_ld16(taddr + c0, v);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[c0 + j] = (cc == 0) ? v[j] : acc[c0 + j] + v[j];
+        }
+        fence_before_sync();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty + 8 * as);
+      }
       if (tile < 0) break;
-      const int mc = (tile % p.tm) * BM, nc = (tile / p.tm) * BN;
-      fence_after_sync();
+      const int mc = (tile % p.tm) * BM, nc = (tile / p.tm) * BN + h * EPI_COLS;
       const int m = mc + q * 32 + lane;
-      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        float v[16];
-        tmem_ld16(taddr + c0, v);
-        if (m < p.M) {
+      if (m < p.M) {
+#pragma unroll
+        for (int c0 = 0; c0 < EPI_COLS; c0 += 16) {
           float cv[16];
           if (p.beta != 0.0f) {
 #pragma unroll
@@ -346,15 +381,12 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int j = 0; j < 16; ++j) {
             const int n = nc + c0 + j;
             if (n < p.N) {
-              const float r = p.alpha * v[j];
+              const float r = p.alpha * acc[c0 + j];
               p.C[m + (long)n * p.ldc] = (p.beta == 0.0f) ? r : fmaf(p.beta, cv[j], r);
             }
           }
         }
       }
-      fence_before_sync();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(acc_empty + 8 * as);
     }
   }
   fence_before_sync();

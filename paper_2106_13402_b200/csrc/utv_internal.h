@@ -70,6 +70,11 @@ int laset(int uplo, int rows, int cols, double alpha, double beta, double* A, lo
 // A <- alpha diag(d) A (side 0) or alpha A diag(d) (side 1).
 int diag_scale(int side, int rows, int cols, const double* d, double alpha, double* A, long lda,
                cudaStream_t st);
+// device generators / metrics (metrics.cu)
+int gen_bie(double* A, long lda, int n, cudaStream_t st);
+int gen_kahan(double* A, long lda, int n, double theta, cudaStream_t st);
+size_t trailing_fro_ws_doubles(int m, int n);
+int trailing_fro(const double* T, long ldt, int m, int n, double* e, double* ws, cudaStream_t st);
 // B (n x m) = A^T (A m x n)
 int transpose(const double* A, long lda, double* B, long ldb, int m, int n, cudaStream_t st);
 // fp32 helpers of the C5 path (ops.cu)

@@ -10,7 +10,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _lib
-from ._lib import DMat, check, dempty, load, stream_ptr, workspace
+from ._lib import DMat, check, dempty, load, stream_ptr, workspace  # noqa: F401
 
 
 def gemm(transa, transb, alpha, A: DMat, B: DMat, beta=0.0, C: DMat | None = None,

@@ -147,8 +147,27 @@ def boosted(uk=None, save=None):
              efro=uk.bench.trailing_fro_curve(f.T), next_normal=nxt, call=call)
 
 
+def matgen():
+    """Reference generators (matgen.py) at small sizes."""
+    sys.dont_write_bytecode = True
+    sys.path.insert(0, REF)
+    import utvkit as uk  # noqa: E402
+    a, d = uk.gen_fast_decay(64, 1e-3, uk.RngStream(71))
+    b, e = uk.gen_s_shaped(48, uk.RngStream(72))
+    q = uk.matgen.random_orthogonal(40, uk.RngStream(73))
+    np.savez_compressed(os.path.join(OUT, "matgen_small.npz"), fast=a, fast_d=d, s=b, s_d=e,
+                        bie=uk.gen_bie(20), kahan=uk.gen_kahan(12), kahan_th=uk.gen_kahan(9, 0.7),
+                        orth=q, gauss=uk.gen_gaussian(10, uk.RngStream(74)),
+                        call="gen_fast_decay(64,1e-3,RngStream(71)); gen_s_shaped(48,RngStream(72)); "
+                             "random_orthogonal(40,RngStream(73)); gen_bie(20); gen_kahan(12); "
+                             "gen_kahan(9,0.7); gen_gaussian(10,RngStream(74))")
+    print("wrote matgen_small.npz")
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "boosted":
         boosted()
+    elif len(sys.argv) > 1 and sys.argv[1] == "matgen":
+        matgen()
     else:
         main()

@@ -1,0 +1,50 @@
+"""GPU generators (matgen drop-in) and device metrics
+against the reference's own generator outputs and the host metrics."""
+import numpy as np
+import pytest
+
+from oracle import utv_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def test_generators_match_reference(golden):
+    import paper_2106_13402_b200 as pk
+    from paper_2106_13402_b200 import matgen as mg
+    g = golden("matgen_small")
+    a, d = mg.gen_fast_decay(64, 1e-3, pk.RngStream(71))
+    assert np.array_equal(d, g["fast_d"])
+    assert np.abs(a - g["fast"]).max() < 1e-13
+    b, e = mg.gen_s_shaped(48, pk.RngStream(72))
+    assert np.array_equal(e, g["s_d"])
+    assert np.abs(b - g["s"]).max() < 1e-13
+    assert np.abs(mg.random_orthogonal(40, pk.RngStream(73)) - g["orth"]).max() < 1e-13
+    assert np.abs(mg.gen_bie(20) - g["bie"]).max() < 1e-15
+    assert np.abs(mg.gen_kahan(12) - g["kahan"]).max() < 1e-15
+    assert np.abs(mg.gen_kahan(9, 0.7) - g["kahan_th"]).max() < 1e-15
+    assert np.array_equal(mg.gen_gaussian(10, pk.RngStream(74)), g["gauss"])
+
+
+@pytest.mark.parametrize("shape", [(2, 2), (50, 30), (257, 257), (1000, 700)])
+def test_trailing_fro_device_matches_host(shape):
+    import paper_2106_13402_b200 as pk
+    from paper_2106_13402_b200._lib import dfrom_numpy
+    from paper_2106_13402_b200.metrics import trailing_fro_curve_device
+    rng = np.random.default_rng(shape[0])
+    t = rng.standard_normal(shape)
+    host = pk.trailing_fro_curve(t)
+    dev = trailing_fro_curve_device(dfrom_numpy(t))
+    assert dev.shape == host.shape
+    assert np.allclose(dev, host, rtol=1e-12, atol=1e-12)
+
+
+def test_device_reconstruction_orthogonality():
+    import paper_2106_13402_b200 as pk
+    from paper_2106_13402_b200._lib import dfrom_numpy
+    from paper_2106_13402_b200.metrics import orthogonality_device, reconstruction_device
+    a, _ = orc.decay_matrix(300, 1e-5, seed=3)
+    f = pk.randutv_basic(a, 64, 1, pk.RngStream(1))
+    r_dev = reconstruction_device(dfrom_numpy(a), dfrom_numpy(f.U), dfrom_numpy(f.T), dfrom_numpy(f.V))
+    assert abs(r_dev - orc.reconstruction(a, f.U, f.T, f.V)) < 1e-15
+    o_dev = orthogonality_device(dfrom_numpy(f.U))
+    assert abs(o_dev - orc.orthogonality(f.U)) < 1e-15
