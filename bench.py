@@ -31,6 +31,12 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FP64_PEAK_TFLOPS = 37.1   # measured DMMA m8n8k4 peak on this pool's B200 (profiles/fp64_peak_r01.json)
+# DRAM traffic of the representative WY-update launch (NT 16384x16384x256,
+# beta=1), one `ncu --set full` capture: read + write bytes per launch vs the
+# algorithmic bytes (A, B 32 MiB each + C read and written, 2 GiB each).
+GEMM_TRAFFIC = {"bytes": 2.853321e9 + 2.101429e9, "algorithmic_bytes": 2 * 8 * 16384 * 256 + 2 * 8 * 16384 ** 2,
+                "launch": "dgemm NT M=N=16384 K=256 beta=1 (compact-WY trailing update)",
+                "source": "profiles/r01_ncu_gemm_nt_16384x16384x256_v3.txt"}
 FP64_PEAK_SRC = "measured: tools/fp64_peak.cu DMMA m8n8k4, 148 SMs @1965 MHz (profiles/fp64_peak_r01.json)"
 
 
@@ -363,7 +369,8 @@ def run_ours(args):
                    "frac_of_fp64_peak": value / ws / FP64_PEAK_TFLOPS},
         "roofline": {"bound": "tensor", "kernel": "dgemm_tma_kernel (DMMA.8x8x4)",
                      "achieved": gemm_tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                     "frac": gemm_tflops / FP64_PEAK_TFLOPS, "traffic": None,
+                     "frac": gemm_tflops / FP64_PEAK_TFLOPS, "traffic": GEMM_TRAFFIC["bytes"],
+                     "traffic_note": GEMM_TRAFFIC,
                      "peak_source": FP64_PEAK_SRC,
                      "share_of_step": g["ms"] / 1e3 / (rutv_s + purv_s),
                      "launches_per_step": g["count"]},

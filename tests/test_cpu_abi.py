@@ -84,3 +84,15 @@ def test_rng_stream_matches_reference_draw_order():
     assert len(blocks) == len(ref) == 4
     for x, y in zip(blocks, ref):
         assert np.array_equal(x, y)
+
+
+def test_cli_usage_and_exit_codes(tmp_path):
+    from paper_2106_13402_b200 import cli
+    assert cli.main(["time"]) == 1                       # missing required args -> usage error
+    assert cli.main(["bogus"]) == 1
+    a = np.arange(12.0).reshape(4, 3) + 0.5
+    p = tmp_path / "a.mtx"
+    cli.write_matrix(a, str(p))
+    assert np.array_equal(cli.read_matrix(str(p)), a)    # %.17g round-trips bitwise
+    # comparators are not on the B200 path: ValueError -> exit 1
+    assert cli.main(["factor", "--algo", "svd", "--in", str(p), "--out-prefix", str(tmp_path / "f")]) == 1

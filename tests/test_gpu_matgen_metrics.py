@@ -48,3 +48,18 @@ def test_device_reconstruction_orthogonality():
     assert abs(r_dev - orc.reconstruction(a, f.U, f.T, f.V)) < 1e-15
     o_dev = orthogonality_device(dfrom_numpy(f.U))
     assert abs(o_dev - orc.orthogonality(f.U)) < 1e-15
+
+
+def test_cli_time_and_factor(tmp_path, capsys):
+    from paper_2106_13402_b200 import cli
+    assert cli.main(["gen", "--kind", "fast", "--n", "120", "--out", str(tmp_path / "a.mtx")]) == 0
+    assert cli.main(["factor", "--algo", "randutv", "--b", "32", "--q", "1", "--in", str(tmp_path / "a.mtx"),
+                     "--out-prefix", str(tmp_path / "f")]) == 0
+    a = cli.read_matrix(str(tmp_path / "a.mtx"))
+    u, t, v = (cli.read_matrix(str(tmp_path / f"f.{x}.mtx")) for x in "UTV")
+    assert np.linalg.norm(a - u @ t @ v.T) / np.linalg.norm(a) < 1e-13
+    assert cli.main(["curve", "--factors", str(tmp_path / "f"), "--csv", str(tmp_path / "e.csv")]) == 0
+    assert cli.main(["time", "--algo", "powerurv", "--n", "200", "--q", "1", "--reps", "2",
+                     "--csv", str(tmp_path / "t.csv")]) == 0
+    out = capsys.readouterr().out
+    assert "powerurv n=200: median" in out
