@@ -30,6 +30,6 @@ if what in ("all", "purv"):
     a, _ = orc.decay_matrix(160, 1e-5, seed=4, m=300)
     pk.power_urv(a, 2, pk.RngStream(2))
     from paper_2106_13402_b200.sharded import Comm, power_urv_sharded
-    power_urv_sharded(dfrom_numpy(a), dfrom_numpy(orc.draw_gaussian(orc.gaussian_stream(1), 160, 160)), 1, Comm(), chunk_rows=170)
+    power_urv_sharded(dfrom_numpy(a), dfrom_numpy(orc.draw_gaussian(orc.gaussian_stream(1), 160, 160)), 1, Comm(), chunk_rows=200)
 torch.cuda.synchronize()
 print("done", what)
