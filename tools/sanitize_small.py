@@ -27,9 +27,9 @@ if what in ("all", "rutv"):
     pk.randutv_boosted(a, 48, 1, 16, pk.RngStream(2))
     pk.randutv_basic(np.asfortranarray(a), 48, 1, pk.RngStream(1), dtype=np.float32)
 if what in ("all", "purv"):
-    a, _ = orc.decay_matrix(160, 1e-5, seed=4, m=300)
+    a, _ = orc.decay_matrix(96, 1e-5, seed=4, m=300)
     pk.power_urv(a, 2, pk.RngStream(2))
     from paper_2106_13402_b200.sharded import Comm, power_urv_sharded
-    power_urv_sharded(dfrom_numpy(a), dfrom_numpy(orc.draw_gaussian(orc.gaussian_stream(1), 160, 160)), 1, Comm(), chunk_rows=200)
+    power_urv_sharded(dfrom_numpy(a), dfrom_numpy(orc.draw_gaussian(orc.gaussian_stream(1), 96, 96)), 1, Comm(), chunk_rows=140)
 torch.cuda.synchronize()
 print("done", what)
