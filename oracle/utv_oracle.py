@@ -247,6 +247,105 @@ def randutv_basic(a, b, q, g_blocks, record_trailing=False):
     return dict(U=u, T=t, V=v, errors=errors, trailing=trailing, steps=steps)
 
 
+def randutv_boosted(a, b, q, p, gen, tol_fro=None, max_rank=None, record_trailing=False):
+    """Boosted / partial randUTV (Algorithm 2; randutv.py:110-182 with
+    boosted=True, _sample_boosted :196-225, svd_tall_thin_left svd.py:61-82).
+
+    ``gen`` is the numpy Generator of the reference's RngStream; draws are
+    made lazily in the reference's order (step 1: m x (b+p), later
+    (m-lo) x b) so an early stop leaves the generator where the reference
+    would.  Returns dict(U, T, V, errors, trailing, steps).
+    """
+    a = np.asarray(a, dtype=np.float64)
+    m, n = a.shape
+    t = np.array(a, order="F", copy=True)
+    u = np.eye(m, order="F")
+    v = np.eye(n, order="F")
+    e0 = float(np.linalg.norm(a))
+    e_sq, e0_sq = e0 * e0, e0 * e0
+    errors, trailing = [], ([] if record_trailing else None)
+    w_next, steps = None, 0
+
+    def track(panel):
+        nonlocal e_sq
+        e_sq -= float(np.sum(panel * panel))
+        if e_sq < -1e-10 * e0_sq:
+            raise OracleError("tracked squared error went negative")
+        e_sq = max(e_sq, 0.0)
+        errors.append(math.sqrt(e_sq))
+
+    for i in range(1, -(-n // b) + 1):
+        if tol_fro is not None and math.sqrt(e_sq) <= tol_fro:          # randutv.py:123-124
+            break
+        lo, mid = (i - 1) * b, (i - 1) * b + b
+        nrows, ncols = m - lo, n - lo
+        if ncols > b + p:
+            blk = t[lo:, lo:]
+            if i == 1:                                                 # randutv.py:205-210
+                y = blk.T @ draw_gaussian(gen, m, b + p)
+                for _ in range(q):
+                    y = blk.T @ (blk @ y)
+            else:                                                      # randutv.py:211-225
+                y = blk.T @ draw_gaussian(gen, nrows, b)
+                for _ in range(q - 1):
+                    y = blk.T @ (blk @ y)
+                x = blk @ y
+                if w_next is not None:
+                    pad = x.shape[0] - w_next.shape[0]
+                    w = np.vstack([w_next, np.zeros((pad, w_next.shape[1]))]) if pad else w_next
+                    x = x - w @ (w.T @ x)
+                else:
+                    w = np.zeros((x.shape[0], 0))
+                qy, qt, _ = householder_qr(x)
+                y = blk.T @ np.hstack([wy_materialize(qy, qt, b), w])
+            # svd_tall_thin_left(y) (svd.py:61-82): W = Q blockdiag(Uhat, I)
+            yy, yt, yr = householder_qr(y)
+            wc = y.shape[1]
+            uhat, _, _ = svd_signed(yr[:wc, :])
+            c = np.zeros((ncols, ncols), order="F")
+            c[:wc, :wc] = uhat
+            if ncols > wc:
+                c[wc:, wc:] = np.eye(ncols - wc)
+            w_y = wy_apply(yy, yt, c, "left")
+            vy, vt, _ = householder_qr(w_y[:, :b])                     # randutv.py:134
+            if p > 0 and (ncols - b) > b + p:                          # randutv.py:135-138
+                w_next = wy_apply(vy, vt, w_y[:, b:b + p], "left", trans=True)[b:, :]
+            else:
+                w_next = None
+            t[:, lo:] = wy_apply(vy, vt, t[:, lo:], "right")
+            v[:, lo:] = wy_apply(vy, vt, v[:, lo:], "right")
+            uy, ut, rp = householder_qr(t[lo:, lo:mid])
+            u[:, lo:] = wy_apply(uy, ut, u[:, lo:], "right")
+            t[lo:, mid:] = wy_apply(uy, ut, t[lo:, mid:], "left", trans=True)
+            t[mid:, lo:mid] = 0.0
+            su, ss, sv = svd_signed(rp[:b, :])
+            u[:, lo:mid] = u[:, lo:mid] @ su
+            v[:, lo:mid] = v[:, lo:mid] @ sv
+            t[lo:mid, lo:mid] = np.diag(ss)
+            t[lo:mid, mid:] = su.T @ t[lo:mid, mid:]
+            t[:lo, lo:mid] = t[:lo, lo:mid] @ sv
+            steps = i
+            track(t[lo:mid, lo:])
+            if trailing is not None:
+                trailing.append(float(np.linalg.norm(t[mid:, mid:])))
+            if max_rank is not None and i * b >= max_rank:
+                break
+        else:
+            su, ss, sv = svd_signed(t[lo:, lo:])
+            u[:, lo:] = u[:, lo:] @ su
+            v[:, lo:] = v[:, lo:] @ sv
+            d = np.zeros((nrows, ncols), order="F")
+            d[np.arange(ss.shape[0]), np.arange(ss.shape[0])] = ss
+            t[lo:, lo:] = d
+            t[:lo, lo:] = t[:lo, lo:] @ sv
+            steps = i
+            track(t[lo:, lo:])
+            if trailing is not None:
+                trailing.append(0.0)
+            break
+    return dict(U=u, T=t, V=v, errors=errors, trailing=trailing, steps=steps)
+
+
 # ---------------------------------------------------------------------------
 # Parity metrics (bench.py:63-72; SURVEY Appendix A.2)
 # ---------------------------------------------------------------------------

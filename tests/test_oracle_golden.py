@@ -81,3 +81,20 @@ def test_randutv_basic_matches_reference(golden, name):
     assert np.abs(f["V"] - g["V"]).max() < 1e-8
     assert np.allclose(f["errors"], g["errors"], rtol=1e-8, atol=1e-7 * np.linalg.norm(a))
     assert orc.reconstruction(a, f["U"], f["T"], f["V"]) < 1e-13
+
+
+@pytest.mark.parametrize("name", sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "boost_*.npz"))))
+def test_oracle_boosted_matches_reference(golden, name):
+    """The boosted / partial restatement against the reference's own outputs,
+    including where the generator is left (next draw)."""
+    g = golden(name)
+    gen = orc.gaussian_stream(int(g["seed"]))
+    tol = None if np.isnan(g["tol"]) else float(g["tol"])
+    mr = None if int(g["max_rank"]) < 0 else int(g["max_rank"])
+    out = orc.randutv_boosted(g["A"], int(g["b"]), int(g["q"]), int(g["p"]), gen, tol_fro=tol,
+                              max_rank=mr, record_trailing=True)
+    assert gen.standard_normal((1, 1))[0, 0] == g["next_normal"]
+    assert out["steps"] == int(g["steps"])
+    assert np.abs(out["T"] - g["T"]).max() < 1e-9 * max(1.0, np.abs(g["T"]).max())
+    assert np.abs(np.diag(out["T"]) - np.diag(g["T"])).max() < 1e-11
+    assert np.allclose(out["errors"], g["errors"], rtol=1e-9, atol=1e-10)
