@@ -79,6 +79,18 @@ int utv_dlarfb(char side, char trans, int m, int n, int k, int w, const double* 
  * inputs are split into row chunks by the caller (TSQR). */
 int utv_dgeqrf_rows_max(void);
 
+/* Column-pivoted Householder QR (HQRCP), replaces hqrcp (qr.py:152-204):
+ * A[:, perm] = Q R with Q = I - Y T Y^T (Y m x r unit lower trapezoidal, T
+ * r x r upper, r = min(m, n)), R m x n in pivoted column order, perm[k] the
+ * original index of column k (0-based, the reference's `perm`).  Greedy
+ * largest-norm pivoting with the reference's 1e-12 tie window (leftmost),
+ * skip rule and norm downdate/recompute.  A is overwritten (working storage).
+ * m, n <= utv_dgeqp3_max_dim(). */
+size_t utv_dgeqp3_bufsize(int m, int n);
+int utv_dgeqp3_max_dim(void);
+int utv_dgeqp3_f64(int m, int n, double* A, long lda, double* R, long ldr, double* Y, long ldy,
+                   double* T, long ldt, int* perm, void* work, size_t lwork, void* stream);
+
 /* Device generators (matgen.py:58-91: gen_bie, gen_kahan) and the Frobenius
  * error curve e_k = ||T[k:, k:]||_F, k = 1..n-1 (bench.py:63-72) -> e (device,
  * n-1 doubles), O(mn), fixed-order (bitwise reproducible). */

@@ -347,6 +347,74 @@ def randutv_boosted(a, b, q, p, gen, tol_fro=None, max_rank=None, record_trailin
 
 
 # ---------------------------------------------------------------------------
+# Column-pivoted QR comparator (qr.py:140-204)
+# ---------------------------------------------------------------------------
+
+PIVOT_TIE_RTOL = 1e-12   # qr.py:148
+DOWNDATE_RTOL = EPS      # qr.py:143
+
+
+def hqrcp(a):
+    """Businger-Golub column-pivoted Householder QR, restating qr.py:152-204.
+
+    Returns (Y m x r, Twy r x r, R m x n in pivoted order, perm), r = min(m, n):
+    greedy largest squared-norm pivot; ties within a 1e-12 relative window go
+    to the leftmost logical column (qr.py:171-175); reflector + skip rule as in
+    householder_qr (qr.py:43-60, 182-194); squared-norm downdate clamped at 0
+    with an exact recompute once the estimate is <= eps * its last exact value
+    (qr.py:196-202).
+    """
+    a = np.asarray(a, dtype=np.float64)
+    m, n = a.shape
+    r = min(m, n)
+    work = np.array(a, order="F", copy=True)
+    vecs = np.zeros((m, r), order="F")
+    tri = np.zeros((r, r), order="F")
+    perm = np.arange(n)
+    cutoff = EPS * float(np.linalg.norm(a))                  # qr.py:162
+    est = np.sum(work * work, axis=0)                        # qr.py:164
+    exact = est.copy()                                       # qr.py:165
+    for j in range(r):
+        rest = est[j:]
+        big = float(rest.max())
+        k = j + int(np.argmax(rest >= big * (1.0 - PIVOT_TIE_RTOL))) if big > 0.0 else j
+        if k != j:                                           # qr.py:176-180
+            work[:, [j, k]] = work[:, [k, j]]
+            perm[[j, k]] = perm[[k, j]]
+            est[[j, k]] = est[[k, j]]
+            exact[[j, k]] = exact[[k, j]]
+        col = work[j:, j].copy()
+        head = float(col[0])
+        tail_sq = float(col[1:] @ col[1:])
+        nrm = math.sqrt(head * head + tail_sq)
+        if nrm <= cutoff or tail_sq == 0.0:                  # skip, qr.py:183-186
+            vecs[j, j] = 1.0
+            work[j + 1:, j] = 0.0
+        else:
+            sgn = 1.0 if head >= 0.0 else -1.0
+            pivot = head + sgn * nrm
+            v = col / pivot
+            v[0] = 1.0
+            tau = 2.0 / (1.0 + tail_sq / (pivot * pivot))
+            w = tau * (v @ work[j:, j:])                     # qr.py:188-189
+            work[j:, j:] -= np.outer(v, w)
+            work[j, j] = -sgn * nrm
+            work[j + 1:, j] = 0.0
+            vecs[j:, j] = v
+            tri[j, j] = tau                                  # qr.py:63-68
+            if j > 0:
+                z = vecs[j:, :j].T @ v
+                tri[:j, j] = -tau * (tri[:j, :j] @ z)
+        if j + 1 < n:                                        # qr.py:196-202
+            est[j + 1:] -= work[j, j + 1:] ** 2
+            np.maximum(est[j + 1:], 0.0, out=est[j + 1:])
+            for c in j + 1 + np.nonzero(est[j + 1:] <= DOWNDATE_RTOL * exact[j + 1:])[0]:
+                est[c] = float(work[j + 1:, c] @ work[j + 1:, c])
+                exact[c] = est[c]
+    return vecs, tri, work, perm
+
+
+# ---------------------------------------------------------------------------
 # Parity metrics (bench.py:63-72; SURVEY Appendix A.2)
 # ---------------------------------------------------------------------------
 

@@ -8,14 +8,14 @@ from .errors import ConsistencyError, ConvergenceError, DimensionError
 from .matrix import MACHINE_EPS, RngStream, check_matrix, frobenius_norm, gaussian
 from .metrics import trailing_fro_curve
 from .powerurv import UrvFactorization, power_urv, power_urv_from_sample, rurv
-from .qr import QFactor, apply_q, hqr_full, hqr_thin, materialize_q
+from .qr import PivotedQr, QFactor, apply_q, hqr_full, hqr_thin, hqrcp, materialize_q
 from .randutv import (ErrorTracker, UtvFactorization, error_update, randutv_basic,
                       randutv_boosted, randutv_partial)
 from .svd import SvdTriple, svd_dense
 
 __all__ = [
     "MACHINE_EPS", "RngStream", "gaussian", "frobenius_norm", "check_matrix",
-    "QFactor", "hqr_full", "hqr_thin", "apply_q", "materialize_q",
+    "QFactor", "PivotedQr", "hqr_full", "hqr_thin", "hqrcp", "apply_q", "materialize_q",
     "SvdTriple", "svd_dense",
     "UrvFactorization", "power_urv", "power_urv_from_sample", "rurv",
     "UtvFactorization", "ErrorTracker", "error_update", "randutv_basic",

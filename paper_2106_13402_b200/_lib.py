@@ -64,6 +64,10 @@ SIGNATURES = {
                                  c_void_p, c_long, c_void_p, c_long, c_void_p, c_long, c_void_p,
                                  c_long, c_void_p, c_long, c_void_p, c_size_t, c_void_p]),
     "utv_dgeqrf_rows_max": (c_int, []),
+    "utv_dgeqp3_bufsize": (c_size_t, [c_int, c_int]),
+    "utv_dgeqp3_max_dim": (c_int, []),
+    "utv_dgeqp3_f64": (c_int, [c_int, c_int, c_void_p, c_long, c_void_p, c_long, c_void_p, c_long,
+                               c_void_p, c_long, c_void_p, c_void_p, c_size_t, c_void_p]),
     "utv_sgemm_tf32x3": (c_int, [c_char, c_char, c_int, c_int, c_int, ctypes.c_float, c_void_p, c_long,
                                  c_void_p, c_long, ctypes.c_float, c_void_p, c_long, c_void_p]),
     "utv_dlacpy": (c_int, [c_int, c_int, c_void_p, c_long, c_void_p, c_long, c_void_p]),
@@ -89,7 +93,7 @@ SIGNATURES = {
 }
 
 PROF_CATEGORIES = ("dgemm_dmma", "splitk_reduce", "panel_qr", "jacobi_rounds",
-                   "jacobi_finish", "small_ops", "sgemm_tf32x3")
+                   "jacobi_finish", "small_ops", "sgemm_tf32x3", "qrcp")
 
 
 def load():

@@ -110,6 +110,23 @@ int utv_dlarfb(char side, char trans, int m, int n, int k, int w, const double* 
 
 int utv_dgeqrf_rows_max(void) { return panel_rows_max(); }
 
+size_t utv_dgeqp3_bufsize(int m, int n) { return B(qrcp_ws_doubles(m, n)); }
+int utv_dgeqp3_max_dim(void) { return qrcp_max_dim(); }
+
+int utv_dgeqp3_f64(int m, int n, double* A, long lda, double* R, long ldr, double* Y, long ldy,
+                   double* T, long ldt, int* perm, void* work, size_t lwork, void* stream) {
+  if (m < 1) return -1;
+  if (n < 1) return -2;
+  const int r = m < n ? m : n;
+  if (!ld_ok(lda, m)) return -4;
+  if (!ld_ok(ldr, m)) return -6;
+  if (!ld_ok(ldy, m)) return -8;
+  if (!ld_ok(ldt, r)) return -10;
+  if (perm == nullptr) return -11;
+  return qrcp(m, n, A, lda, R, ldr, Y, ldy, T, ldt, perm, (double*)work, lwork / sizeof(double),
+              S(stream));
+}
+
 int utv_randutv_basic_steps_f64(int i0, int i1, int m, int n, int b, int q, double* T, long ldt,
                                 double* U, long ldu, double* V, long ldv, const double* G, long ldg,
                                 double* errsq, double* trail2, int* svd_status, void* work,

@@ -25,7 +25,8 @@ enum ProfCat {
   PROF_JFINISH = 4,   // Jacobi finish kernel
   PROF_OPS = 5,       // reductions / structured writes / copies
   PROF_GEMM_TF32 = 6, // 3xTF32 tcgen05 GEMM (flops = 2MNK useful)
-  PROF_NCAT = 7
+  PROF_QRCP = 7,      // column-pivoted QR kernel (HBM-bound, bytes = trailing read + write)
+  PROF_NCAT = 8
 };
 struct ProfScope {
   ProfScope(int cat, double flops, double bytes, cudaStream_t st, int launches = 1);
@@ -125,6 +126,12 @@ int orgqr_panels(Mat Y, Mat T, Mat Q, double* ws, size_t ws_doubles, cudaStream_
 // forward compact-WY triangle of the whole product (qr.py:63-68 semantics).
 size_t build_t_ws_doubles(int rows, int cols);
 int build_t(Mat Y, Mat T, double* ws, size_t ws_doubles, cudaStream_t st);
+
+// ---- column-pivoted QR comparator (qrcp.cu), qr.py:152-204 ----
+int qrcp_max_dim();
+size_t qrcp_ws_doubles(int m, int n);
+int qrcp(int m, int n, double* A, long lda, double* R, long ldr, double* Y, long ldy, double* T,
+         long ldt, int* perm, double* ws, size_t ws_doubles, cudaStream_t st);
 
 // ---- Householder reconstruction for TSQR (lu.cu) ----
 // In-place LU without pivoting of (P - diag(s)), rows >= cols, s_j = -sign(pivot_j).

@@ -69,6 +69,27 @@ def geqrf(A: DMat):
     return Y, T
 
 
+def geqp3(A: DMat):
+    """Column-pivoted QR (utv_dgeqp3_f64); A is destroyed. Returns (R, Y, T, perm)."""
+    import torch
+    lib = load()
+    m, n = A.rows, A.cols
+    r = min(m, n)
+    R = dempty(m, n)
+    Y = dempty(m, r)
+    T = dempty(r, r)
+    perm = torch.empty(n, dtype=torch.int32, device="cuda")
+    lw = lib.utv_dgeqp3_bufsize(m, n)
+    ws = workspace(lw)
+    check(lib.utv_dgeqp3_f64(m, n, A.ptr, A.ld, R.ptr, R.ld, Y.ptr, Y.ld, T.ptr, T.ld,
+                             perm.data_ptr(), ws.data_ptr(), lw, stream_ptr()), "utv_dgeqp3_f64")
+    return R, Y, T, perm
+
+
+def geqp3_max_dim():
+    return int(load().utv_dgeqp3_max_dim())
+
+
 def larfb(side, trans, Y: DMat, T: DMat, B: DMat):
     lib = load()
     lw = lib.utv_dlarfb_bufsize(B.rows, B.cols, Y.cols)

@@ -28,6 +28,15 @@ class QFactor:
         return self.Y.shape[1]
 
 
+@dataclass(frozen=True)
+class PivotedQr:
+    """Column-pivoted QR: ``A[:, perm] = Q @ R`` with |diag R| non-increasing (qr.py:35-40)."""
+
+    q: QFactor
+    R: np.ndarray
+    perm: np.ndarray
+
+
 def hqr_full(a):
     """Full unpivoted Householder QR (m >= n) -> (QFactor, R); qr.py:71-100."""
     a = check_matrix(a)
@@ -72,3 +81,19 @@ def hqr_thin(a):
     q, r = hqr_full(a)
     n = np.asarray(a).shape[1]
     return materialize_q(q, ncols=n), np.array(r[:n, :], copy=True)
+
+
+def hqrcp(a):
+    """Column-pivoted Householder QR (greedy largest-norm pivoting) — the
+    paper's comparator, qr.py:152-204, as one persistent cooperative kernel
+    (csrc/qrcp.cu).  Same pivots (1e-12 tie window, leftmost), skip rule and
+    norm downdate/recompute as the reference; any m x n up to the device
+    limit (utv_dgeqp3_max_dim, 16384 per side)."""
+    a = check_matrix(a)
+    m, n = a.shape
+    lim = dv.geqp3_max_dim()
+    if m > lim or n > lim:
+        raise DimensionError(f"hqrcp on the B200 path supports up to {lim} rows/cols, got {a.shape}")
+    R, Y, T, perm = dv.geqp3(dfrom_numpy(a))
+    return PivotedQr(q=QFactor(Y=Y.to_numpy(), Twy=T.to_numpy(), m=m), R=R.to_numpy(),
+                     perm=perm.cpu().numpy().astype(np.int64))

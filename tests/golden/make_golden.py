@@ -164,8 +164,40 @@ def matgen():
     print("wrote matgen_small.npz")
 
 
+def hqrcp():
+    """Reference hqrcp (qr.py:152-204) on pivot-sensitive inputs."""
+    sys.dont_write_bytecode = True
+    sys.path.insert(0, REF)
+    import utvkit as uk  # noqa: E402
+    rng = np.random.default_rng(91)
+    cases = {}
+    cases["gauss120x80"] = rng.standard_normal((120, 80))
+    cases["wide60x90"] = rng.standard_normal((60, 90))
+    cases["kahan100"] = uk.gen_kahan(100, 1.2)
+    cases["fast100"] = uk.gen_fast_decay(100, 1e-9, uk.RngStream(92))[0]
+    rd = rng.standard_normal((80, 60))
+    rd[:, 3] = 0.0                          # zero column
+    rd[:, 7] = rd[:, 1]                     # exact duplicate -> tie, leftmost wins
+    rd[:, 11] = -rd[:, 1]
+    rd[:, 20] = rd[:, 2] + 1e-9 * rd[:, 5]  # near-dependent -> downdate recompute
+    rd[:, 40:] = rd[:, :20] @ rng.standard_normal((20, 20))  # rank 40ish
+    cases["rankdef80x60"] = rd
+    cases["equalcols30x12"] = np.ones((30, 12))
+    cases["one1x1"] = np.array([[-2.5]])
+    cases["row1x5"] = rng.standard_normal((1, 5))
+    cases["col5x1"] = rng.standard_normal((5, 1))
+    cases["zero6x4"] = np.zeros((6, 4))
+    for name, a in cases.items():
+        f = uk.hqrcp(a)
+        np.savez_compressed(os.path.join(OUT, f"qrcp_{name}.npz"), a=a, Y=f.q.Y, Twy=f.q.Twy, R=f.R,
+                            perm=f.perm, call="hqrcp(a)")
+        print("wrote", name)
+
+
 if __name__ == "__main__":
-    if len(sys.argv) > 1 and sys.argv[1] == "boosted":
+    if len(sys.argv) > 1 and sys.argv[1] == "hqrcp":
+        hqrcp()
+    elif len(sys.argv) > 1 and sys.argv[1] == "boosted":
         boosted()
     elif len(sys.argv) > 1 and sys.argv[1] == "matgen":
         matgen()

@@ -1,0 +1,105 @@
+"""GPU parity of the column-pivoted QR comparator (hqrcp, qr.py:152-204;
+csrc/qrcp.cu) with the reference's golden vectors and the CPU oracle.
+
+Gate: the permutation must be IDENTICAL (pivot choices are integer results);
+R, Y, Twy to roundoff (1e-11 relative to the largest entry, plus the mixed
+absolute floor for entries at the noise level)."""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from oracle import utv_oracle as orc
+from tests.conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+def _names(prefix):
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, prefix + "*.npz")))
+
+
+def _check(f, y, t, r, perm, a):
+    scale = max(1.0, np.abs(r).max())
+    assert (f.perm == perm).all(), np.nonzero(f.perm != perm)[0][:10]
+    assert f.R.shape == r.shape and f.q.Y.shape == y.shape and f.q.Twy.shape == t.shape
+    assert np.abs(f.R - r).max() <= 1e-11 * scale
+    assert np.abs(f.q.Y - y).max() <= 1e-10
+    assert np.abs(f.q.Twy - t).max() <= 1e-10
+    # exact structure: zeros below diag(R) in the pivoted columns, unit-lower Y
+    k = min(a.shape)
+    assert not np.tril(f.R[:, :k], -1).any()
+    assert not np.triu(f.q.Y, 1).any()
+    assert (np.diag(f.q.Y) == 1.0).all()
+
+
+def _stable_prefix(r):
+    """Pivot steps whose column norm is above the downdating noise floor.
+    Downdated squared norms carry an absolute error ~eps*||a_c||^2, so once
+    |R_kk| falls to ~sqrt(eps)*|R_00| the reference's own pivots change under
+    a 1-ulp perturbation of A (measured on qrcp_fast100: steps 94-98 reorder);
+    below 1e-6*|R_00| only the invariants are gated."""
+    d = np.abs(np.diag(r))
+    return int(np.sum(d > 1e-6 * d[0])) if d.size and d[0] > 0 else 0
+
+
+@pytest.mark.parametrize("name", _names("qrcp_"))
+def test_hqrcp_matches_reference_golden(golden, name):
+    import paper_2106_13402_b200 as pk
+    g = golden(name)
+    a = g["a"]
+    f = pk.hqrcp(a)
+    if (f.perm == g["perm"]).all():
+        _check(f, g["Y"], g["Twy"], g["R"], g["perm"], a)
+    else:
+        p = _stable_prefix(g["R"])
+        assert (f.perm[:p] == g["perm"][:p]).all()
+        scale = max(1.0, np.abs(g["R"]).max())
+        assert np.abs(f.R[:, :p] - g["R"][:, :p]).max() <= 1e-11 * scale
+        assert np.abs(f.q.Y[:, :p] - g["Y"][:, :p]).max() <= 1e-10
+        assert np.abs(f.q.Twy[:p, :p] - g["Twy"][:p, :p]).max() <= 1e-10
+    q = orc.wy_materialize(f.q.Y, f.q.Twy)
+    assert np.linalg.norm(a[:, f.perm] - q @ f.R) <= 1e-14 * max(1.0, np.linalg.norm(a)) * 10
+    d = np.abs(np.diag(f.R))
+    assert (d[1:] <= d[:-1] * (1 + 1e-10) + 1e-6 * (d[0] if d.size else 0)).all()
+
+
+@pytest.mark.parametrize("m,n,seed", [(1500, 1300, 1), (300, 500, 2), (5000, 200, 3), (257, 257, 4)])
+def test_hqrcp_matches_oracle(m, n, seed):
+    """All three register tilings (rows <= 1024 / 4096 / 16384 per column)."""
+    import paper_2106_13402_b200 as pk
+    rng = np.random.default_rng(seed)
+    a = rng.standard_normal((m, n)) * np.exp(-np.arange(n) / (n / 8.0))[None, :]
+    a = a[:, rng.permutation(n)]
+    y, t, r, perm = orc.hqrcp(a)
+    f = pk.hqrcp(a)
+    _check(f, y, t, r, perm, a)
+
+
+def test_hqrcp_invariants_4096():
+    """Size-independent properties at a larger size: A[:, perm] = Q R to
+    roundoff, Q orthogonal, |diag R| non-increasing (greedy pivoting)."""
+    import torch
+    import paper_2106_13402_b200 as pk
+    n = 4096
+    rng = np.random.default_rng(7)
+    a = rng.standard_normal((n, n))
+    f = pk.hqrcp(a)
+    assert sorted(f.perm.tolist()) == list(range(n))
+    q = pk.materialize_q(f.q)
+    qt = torch.from_numpy(q).cuda()
+    at = torch.from_numpy(a[:, f.perm]).cuda()
+    rt = torch.from_numpy(f.R).cuda()
+    rec = float(torch.linalg.norm(at - qt @ rt) / torch.linalg.norm(at))
+    orth = float(torch.linalg.norm(qt.T @ qt - torch.eye(n, dtype=torch.float64, device="cuda")))
+    assert rec < 1e-13, rec
+    assert orth < 1e-11, orth
+    d = np.abs(np.diag(f.R))
+    assert (d[1:] <= d[:-1] * (1 + 1e-10)).all()
+
+
+def test_hqrcp_device_limit_raises():
+    import paper_2106_13402_b200 as pk
+    with pytest.raises(pk.DimensionError):
+        pk.hqrcp(np.ones((16385, 1)))

@@ -98,3 +98,16 @@ def test_oracle_boosted_matches_reference(golden, name):
     assert np.abs(out["T"] - g["T"]).max() < 1e-9 * max(1.0, np.abs(g["T"]).max())
     assert np.abs(np.diag(out["T"]) - np.diag(g["T"])).max() < 1e-11
     assert np.allclose(out["errors"], g["errors"], rtol=1e-9, atol=1e-10)
+
+
+@pytest.mark.parametrize("name", _names("qrcp_"))
+def test_oracle_hqrcp_matches_reference(golden, name):
+    """Column-pivoted QR restatement (qr.py:152-204): identical pivots, and the
+    factors to roundoff, on tie / skip / recompute / wide / degenerate inputs."""
+    g = golden(name)
+    y, t, r, perm = orc.hqrcp(g["A"] if "A" in g else g["a"])
+    assert (perm == g["perm"]).all()
+    scale = max(1.0, np.abs(g["R"]).max())
+    assert np.abs(r - g["R"]).max() <= 1e-13 * scale
+    assert np.abs(y - g["Y"]).max() <= 1e-12
+    assert np.abs(t - g["Twy"]).max() <= 1e-12

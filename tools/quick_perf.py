@@ -55,4 +55,13 @@ if "rutv" in which:
             run.run(T, U, V, G)
         t = ev_time(f, 2)
         out[f"randutv_{n}_b{b}_q{q}"] = dict(s=t, sweeps=run.status.cpu().tolist()[:4]); print(n, b, q, out[f"randutv_{n}_b{b}_q{q}"], flush=True)
+if "qrcp" in which:
+    for n in [1024, 4096, 8192, 16384]:
+        A = rnd(n, n)
+        def f():
+            B = dempty(n, n); B.t.copy_(A.t); dv.geqp3(B)
+        t = ev_time(f, 2)
+        by = sum(16.0 * (n - j) * (n - j - 1) for j in range(n))
+        out[f"geqp3_{n}"] = dict(s=t, gbs=by / t / 1e9); print("geqp3", n, out[f"geqp3_{n}"], flush=True)
+        del A
 print(json.dumps(out, indent=1))
