@@ -26,6 +26,8 @@
 //    T12 = -T11 (Y1^T Y2) T22 row by row (one warp per row, no barriers).
 //  All reductions are in a fixed order: results are bitwise reproducible.
 #include "common.cuh"
+#include <cstdlib>
+
 #include "utv_internal.h"
 
 namespace utv {
@@ -418,6 +420,11 @@ static bool g_panel_attr = false;
 
 int panel_qr(Mat P, Mat Y, Mat T, const double* fro2, double* ws, cudaStream_t st, int max_ctas) {
   if (P.cols > pqr::PW || P.cols < 1 || P.rows < P.cols) return -1;
+  static const int env_ctas = [] {
+    const char* e = getenv("UTV_PANEL_CTAS");  // diagnostics: CTA budget of full-width panels
+    return e ? atoi(e) : 0;
+  }();
+  if (max_ctas == 0 && env_ctas > 0) max_ctas = env_ctas;
   int rc, G;
   pqr::geometry(P.rows, &rc, &G, max_ctas);
   if (rc > pqr::RC_MAX) pqr::geometry(P.rows, &rc, &G, 0);  // too tall for the budget: all SMs

@@ -14,6 +14,9 @@
 // materialised panel by panel (larfb_panels / orgqr_panels), which is what
 // brings the executed FLOPs down to the algorithmic count of SURVEY §8d.
 #include "common.cuh"
+#include <cstdio>
+#include <cstdlib>
+
 #include "utv_internal.h"
 
 namespace utv {
@@ -60,6 +63,18 @@ int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, M
   if (ws_doubles < plan_purv(m, n, nullptr, nullptr)) return UTV_ERR_WORKSPACE;
   PurvWs w;
   plan_purv(m, n, &w, ws);
+  // UTV_PHASES=1: per-phase device times on stderr (diagnostics only)
+  static const bool phases = getenv("UTV_PHASES") != nullptr;
+  cudaEvent_t pev[32];
+  const char* pname[32];
+  int np = 0;
+  auto mark = [&](const char* name) {
+    if (!phases || np >= 32) return;
+    cudaEventCreate(&pev[np]);
+    cudaEventRecord(pev[np], st);
+    pname[np++] = name;
+  };
+  mark("start");
   if (q == 0) {
     // Vq = hqr_full(G) (powerurv.py:58-59); G is read-only -> work on a copy
     UTV_CHECK(copy_mat(G.p, G.ld, w.Yn, w.ldn, n, n, st));
@@ -72,31 +87,50 @@ int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, M
       // Yhat = A V (powerurv.py:64)
       UTV_CHECK(dgemm(false, false, m, n, n, 1.0, A.p, A.ld, vcur, ldv, 0.0, w.Yh, w.ldm, w.gws,
                       SPLITK_WS, st));
+      mark("A*V");
       // Vhat = thin Q of Yhat (powerurv.py:65); any stable thin QR gives the
       // same hqr_full(Y) below (Householder vectors are invariant under the
       // column signs of Vhat), so panel-blocked form suffices.
       Mat Yq{w.Yq, w.ldm, m, n}, Tq{w.Tq, w.ldn, n, n};
       UTV_CHECK(geqrf(Mat{w.Yh, w.ldm, m, n}, Yq, Tq, false, w.qr, w.qr_n, st));
+      mark("geqrf(Yhat)");
       UTV_CHECK(orgqr_panels(Yq, Tq, Mat{w.Vh, w.ldm, m, n}, w.lfb, w.lfb_n, st));
+      mark("orgqr(Vhat)");
       // Y = A^T Vhat (powerurv.py:66)
       UTV_CHECK(dgemm(true, false, n, n, m, 1.0, A.p, A.ld, w.Vh, w.ldm, 0.0, w.Yn, w.ldn, w.gws,
                       SPLITK_WS, st));
+      mark("A^T*Vhat");
       // Vq = hqr_full(Y) (powerurv.py:67); dense T only for the returned factor
       UTV_CHECK(geqrf(Mat{w.Yn, w.ldn, n, n}, Vy, Vt, false, w.qr, w.qr_n, st));
+      mark("geqrf(Y)");
       if (!last) {
         UTV_CHECK(orgqr_panels(Vy, Vt, Mat{w.Vc, w.ldn, n, n}, w.lfb, w.lfb_n, st));
+        mark("orgqr(V)");
         vcur = w.Vc;
         ldv = w.ldn;
       }
     }
     UTV_CHECK(build_t(Vy, Vt, w.bt, w.bt_n, st));
+    mark("build_t(V)");
   }
   // Ahat = A Q(Vq) (powerurv.py:70), formed in R's storage, panel by panel
   UTV_CHECK(copy_mat(A.p, A.ld, R.p, R.ld, m, n, st));
   UTV_CHECK(larfb_panels('R', false, Vy, Vt, R, w.lfb, w.lfb_n, st));
+  mark("A*Q(V)");
   // (Uq, R) = hqr_full(Ahat) (powerurv.py:71)
   UTV_CHECK(geqrf(R, Uy, Ut, false, w.qr, w.qr_n, st));
+  mark("geqrf(Ahat)");
   UTV_CHECK(build_t(Uy, Ut, w.bt, w.bt_n, st));
+  mark("build_t(U)");
+  if (phases) {
+    cudaEventSynchronize(pev[np - 1]);
+    for (int i = 1; i < np; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, pev[i - 1], pev[i]);
+      fprintf(stderr, "[powerurv phase] %-14s %9.3f ms\n", pname[i], ms);
+    }
+    for (int i = 0; i < np; ++i) cudaEventDestroy(pev[i]);
+  }
   return UTV_OK;
 }
 

@@ -130,6 +130,10 @@ static int geqrf_blocked(Mat P, Mat Y, Mat T, bool want_t, const double* fro2, A
     const int v = e ? atoi(e) : 0;
     return v > 0 ? v : 48;
   }();
+  static const int LA_ADAPT = [] {
+    const char* e = getenv("UTV_LA_ADAPT");  // tuning knob: wide width below which the panel gets all SMs
+    return e ? atoi(e) : 0;
+  }();
   bool factored = false;  // panel j0 already factored (look-ahead) on sa
   for (int j0 = 0; j0 < cols; j0 += blk) {
     const int jb = cols - j0 < blk ? cols - j0 : blk;
@@ -153,7 +157,8 @@ static int geqrf_blocked(Mat P, Mat Y, Mat T, bool want_t, const double* fro2, A
         UTV_CUDA(cudaStreamWaitEvent(sa, ev_narrow, 0));
         UTV_CHECK(set_zero(Y.at(0, j1), Y.ld, j1, jb1, sa));
         UTV_CHECK(panel_qr(P.sub(j1, j1, rows - j1, jb1), Y.sub(j1, j1, rows - j1, jb1),
-                           T.sub(j1, j1, jb1, jb1), fro2, pws, sa, LA_CTAS));
+                           T.sub(j1, j1, jb1, jb1), fro2, pws, sa,
+                           (cols - j1 - jb1) < LA_ADAPT ? 0 : LA_CTAS));
         UTV_CUDA(cudaEventRecord(ev_panel, sa));
         factored = true;
         UTV_CHECK(larfb('L', true, Yp, Tp, P.sub(j0, j1 + jb1, rows - j0, cols - j1 - jb1), lfb,

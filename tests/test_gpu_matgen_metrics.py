@@ -63,3 +63,15 @@ def test_cli_time_and_factor(tmp_path, capsys):
                      "--csv", str(tmp_path / "t.csv")]) == 0
     out = capsys.readouterr().out
     assert "powerurv n=200: median" in out
+
+
+def test_cli_cpqr_factor(tmp_path):
+    """cli.py:65-68 semantics for the GPU comparator: U = Q, T = R, V = I[:, perm]."""
+    from paper_2106_13402_b200 import cli
+    assert cli.main(["gen", "--kind", "kahan", "--n", "60", "--out", str(tmp_path / "k.mtx")]) == 0
+    assert cli.main(["factor", "--algo", "cpqr", "--in", str(tmp_path / "k.mtx"),
+                     "--out-prefix", str(tmp_path / "c")]) == 0
+    a = cli.read_matrix(str(tmp_path / "k.mtx"))
+    u, t, v = (cli.read_matrix(str(tmp_path / f"c.{x}.mtx")) for x in "UTV")
+    assert np.linalg.norm(a - u @ t @ v.T) / np.linalg.norm(a) < 1e-13
+    assert np.abs(np.tril(t, -1)).max() == 0.0
