@@ -33,6 +33,24 @@
 namespace utv {
 
 namespace pqr {
+// Diagnostics: build with -DPANEL_PROBE (tools/panel_probe.cu) to accumulate
+// CTA 0's per-phase %globaltimer durations into g_probe.
+#ifdef PANEL_PROBE
+__device__ unsigned long long g_probe[16];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+  return v;
+}
+#define PROBE(k)                                   \
+  if (blockIdx.x == 0 && threadIdx.x == 0) {       \
+    const unsigned long long now_ = gtime();       \
+    g_probe[k] += now_ - probe_last;               \
+    probe_last = now_;                             \
+  }
+#else
+#define PROBE(k)
+#endif
 constexpr int NB = 32;
 constexpr int THREADS = 256;
 constexpr int RC_MIN = 64;
@@ -87,6 +105,9 @@ __global__ void __launch_bounds__(THREADS, 1) panel_qr_kernel(Args a) {
   const double thr = EPS * sqrt(*a.fro2);
   const int nleaf = (cols + NB - 1) / NB;
   unsigned nbar = 0;
+#ifdef PANEL_PROBE
+  unsigned long long probe_last = gtime();
+#endif
   int step = 0;  // global column-step counter (partials double buffer)
   auto gsync = [&]() {
     ++nbar;
@@ -137,6 +158,7 @@ __global__ void __launch_bounds__(THREADS, 1) panel_qr_kernel(Args a) {
     }
     for (int idx = t; idx < NB * (NB + 1); idx += THREADS) Ts[idx] = 0.0;
     __syncthreads();
+    PROBE(0);
 
     // ---- column steps ----
     for (int jj = 0; jj < jb; ++jj, ++step) {
@@ -164,9 +186,11 @@ __global__ void __launch_bounds__(THREADS, 1) panel_qr_kernel(Args a) {
         }
         a.part[((size_t)par * G + g) * 2 * NB + t] = s;
       }
+      PROBE(1);
       garrive();
       ts_column();  // previous column's triangle entries, hidden behind the barrier
       gwait();
+      PROBE(2);
       {  // every CTA: sum the G records, 4 interleaved groups, all loads in flight, fixed order
         const int e = t & 63, q0 = t >> 6;
         double v[PMAX];
@@ -188,6 +212,7 @@ __global__ void __launch_bounds__(THREADS, 1) panel_qr_kernel(Args a) {
       }
       __syncthreads();
 
+      PROBE(3);
       const double sigma = Sv[jj], alpha = Rv[jj];
       const double xnorm = sqrt(alpha * alpha + sigma);
       const bool skip = (xnorm <= thr) || (sigma == 0.0);
@@ -222,9 +247,11 @@ __global__ void __launch_bounds__(THREADS, 1) panel_qr_kernel(Args a) {
         for (int i = i_lo + t; i < nr; i += THREADS) tile[i + jj * ld] = 0.0;
       }
       __syncthreads();
+      PROBE(11);
     }
     ts_column();  // last column of the leaf
     __syncthreads();
+    PROBE(4);
 
     // ---- write R / Y of the leaf; turn the tile into Y form ----
     for (int idx = t; idx < nr * jb; idx += THREADS) {
@@ -247,6 +274,7 @@ __global__ void __launch_bounds__(THREADS, 1) panel_qr_kernel(Args a) {
     if (nX <= 0) continue;     // single-leaf panel: nothing else to do
     const int i0 = max(0, j0 - r0);  // first slab row with Y_leaf possibly != 0
 
+    PROBE(5);
     // ---- phase A: partials of Y_leaf^T X over this slab ----
     for (int cb = 0; cb < nX; cb += XC) {
       const int ncb = min(XC, nX - cb);
@@ -287,7 +315,9 @@ __global__ void __launch_bounds__(THREADS, 1) panel_qr_kernel(Args a) {
           if (jq + x < jb && c < ncb) a.wpart[((size_t)g * NB + jq + x) * PW + cb + c] = acc[x][d];
         }
     }
+    PROBE(6);
     gsync();
+    PROBE(7);
 
     // ---- phase C: reduce the partials across CTAs (8 lanes per entry) ----
     {
@@ -312,7 +342,9 @@ __global__ void __launch_bounds__(THREADS, 1) panel_qr_kernel(Args a) {
         }
       }
     }
+    PROBE(8);
     gsync();
+    PROBE(9);
 
     // ---- phase D: P_trail -= Y_leaf (T_leaf^T W), slab-local ----
     const int nT = cols - j0 - jb;
@@ -358,8 +390,10 @@ __global__ void __launch_bounds__(THREADS, 1) panel_qr_kernel(Args a) {
       }
       __syncthreads();
     }
+    PROBE(13);
   }
 
+  PROBE(10);
   // ---- T off-diagonal blocks: T12 = -T11 (Y1^T Y2) T22, one warp per row ----
   // Leaf by leaf: every CTA stages S[:j0L, leaf L] and T_LL in smem, then its
   // warps finish entries T[r, leaf L] of their rows (a row's earlier entries
@@ -396,6 +430,7 @@ __global__ void __launch_bounds__(THREADS, 1) panel_qr_kernel(Args a) {
       __syncthreads();
     }
   }
+  PROBE(12);
 }
 
 inline void geometry(int rows, int* rc, int* G, int max_ctas) {
