@@ -202,11 +202,14 @@ int utv_powerurv_f64(int m, int n, int q, const double* A, long lda, const doubl
  * utv_launch_count: number of libutvb200 kernel launches since load.
  * utv_profile_begin/end: bracket launches with CUDA events; end() syncs the
  * device and fills per-category totals (categories: 0 DMMA GEMM, 1 split-K
- * reduce, 2 panel-QR leaf, 3 Jacobi rounds, 4 Jacobi finish, 5 small ops);
- * returns the number of categories. */
+ * reduce, 2 panel-QR leaf, 3 Jacobi rounds, 4 Jacobi finish, 5 small ops,
+ * 6 3xTF32 GEMM, 7 column-pivoted QR); returns the number of categories.
+ * utv_profile_busy: per-category union of the launch intervals across all
+ * streams (ms) of the last utv_profile_end — concurrent launches counted once. */
 long long utv_launch_count(void);
 void utv_profile_begin(void);
 int utv_profile_end(double* ms, double* flops, double* bytes, long long* count);
+int utv_profile_busy(double* busy_ms);
 
 #ifdef __cplusplus
 }

@@ -90,6 +90,7 @@ SIGNATURES = {
     "utv_launch_count": (ctypes.c_longlong, []),
     "utv_profile_begin": (None, []),
     "utv_profile_end": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "utv_profile_busy": (c_int, [c_void_p]),
 }
 
 PROF_CATEGORIES = ("dgemm_dmma", "splitk_reduce", "panel_qr", "jacobi_rounds",
@@ -301,7 +302,10 @@ def profile_end():
     by = (ctypes.c_double * n)()
     ct = (ctypes.c_longlong * n)()
     load().utv_profile_end(ms, fl, by, ct)
-    return {PROF_CATEGORIES[i]: dict(ms=ms[i], flops=fl[i], bytes=by[i], count=int(ct[i]))
+    busy = (ctypes.c_double * n)()
+    load().utv_profile_busy(busy)
+    return {PROF_CATEGORIES[i]: dict(ms=ms[i], busy_ms=busy[i], flops=fl[i], bytes=by[i],
+                                     count=int(ct[i]))
             for i in range(n)}
 
 

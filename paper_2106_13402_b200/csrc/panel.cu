@@ -452,6 +452,8 @@ size_t panel_ws_doubles() {
 int panel_rows_max() { return pqr::RC_MAX * pqr::GMAX; }
 
 static bool g_panel_attr = false;
+static thread_local int g_panel_budget = 0;
+void panel_set_max_ctas(int n) { g_panel_budget = n; }
 
 int panel_qr(Mat P, Mat Y, Mat T, const double* fro2, double* ws, cudaStream_t st, int max_ctas) {
   if (P.cols > pqr::PW || P.cols < 1 || P.rows < P.cols) return -1;
@@ -459,6 +461,7 @@ int panel_qr(Mat P, Mat Y, Mat T, const double* fro2, double* ws, cudaStream_t s
     const char* e = getenv("UTV_PANEL_CTAS");  // diagnostics: CTA budget of full-width panels
     return e ? atoi(e) : 0;
   }();
+  if (max_ctas == 0) max_ctas = g_panel_budget;
   if (max_ctas == 0 && env_ctas > 0) max_ctas = env_ctas;
   int rc, G;
   pqr::geometry(P.rows, &rc, &G, max_ctas);

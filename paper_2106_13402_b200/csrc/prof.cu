@@ -5,8 +5,10 @@
 // events brackets the launch on its own stream so bench.py can report the
 // device time, algorithmic FLOPs and bytes of each kernel family (the
 // roofline inputs) without a profiler attached.
+#include <algorithm>
 #include <atomic>
 #include <mutex>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -25,6 +27,8 @@ bool g_on = false;
 std::vector<Rec> g_recs;
 std::vector<cudaEvent_t> g_pool;
 std::atomic<long long> g_launches{0};
+cudaEvent_t g_ref = nullptr;       // timestamp origin of the profiled region
+double g_busy[PROF_NCAT] = {0.0};  // union of launch intervals per category (ms)
 
 cudaEvent_t get_event() {
   if (!g_pool.empty()) {
@@ -67,6 +71,8 @@ void utv_profile_begin(void) {
   std::lock_guard<std::mutex> lk(g_mu);
   g_on = true;
   g_recs.clear();
+  if (!g_ref) cudaEventCreate(&g_ref);
+  cudaEventRecord(g_ref, 0);
 }
 
 // Synchronises the device, then returns per-category totals:
@@ -78,9 +84,13 @@ int utv_profile_end(double* ms, double* flops, double* bytes, long long* count) 
     ms[c] = flops[c] = bytes[c] = 0.0;
     count[c] = 0;
   }
+  std::vector<std::pair<float, float>> iv[PROF_NCAT];
   for (auto& r : g_recs) {
-    float t = 0.f;
+    float t = 0.f, t0 = 0.f, t1 = 0.f;
     cudaEventElapsedTime(&t, r.a, r.b);
+    if (cudaEventElapsedTime(&t0, g_ref, r.a) == cudaSuccess &&
+        cudaEventElapsedTime(&t1, g_ref, r.b) == cudaSuccess)
+      iv[r.cat].push_back({t0, t1});
     ms[r.cat] += t;
     flops[r.cat] += r.flops;
     bytes[r.cat] += r.bytes;
@@ -88,8 +98,34 @@ int utv_profile_end(double* ms, double* flops, double* bytes, long long* count) 
     g_pool.push_back(r.a);
     g_pool.push_back(r.b);
   }
+  // busy time = union of the category's launch intervals over all streams:
+  // concurrent launches (the side-stream transforms) are not double-counted
+  for (int c = 0; c < PROF_NCAT; ++c) {
+    auto& v = iv[c];
+    std::sort(v.begin(), v.end());
+    double busy = 0.0, cs = -1.0, ce = -1.0;
+    for (auto& x : v) {
+      if (x.first > ce) {
+        if (ce > cs) busy += ce - cs;
+        cs = x.first;
+        ce = x.second;
+      } else if (x.second > ce) {
+        ce = x.second;
+      }
+    }
+    if (ce > cs) busy += ce - cs;
+    g_busy[c] = busy;
+  }
   g_recs.clear();
   g_on = false;
+  return PROF_NCAT;
+}
+
+// Per-category busy time (ms) of the last utv_profile_end: the union of the
+// launch intervals across streams.  Returns PROF_NCAT.
+int utv_profile_busy(double* busy_ms) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (int c = 0; c < PROF_NCAT; ++c) busy_ms[c] = g_busy[c];
   return PROF_NCAT;
 }
 

@@ -16,6 +16,8 @@
 #include <mutex>
 
 #include "common.cuh"
+#include <cstdlib>
+
 #include "utv_internal.h"
 
 namespace utv {
@@ -23,6 +25,7 @@ namespace utv {
 struct RutvWs {
   double *Y, *Z, *X, *Bs, *W, *Yv, *Tv, *Yu, *Tu, *Yy, *Ty, *Cs, *sig, *Us, *Vs, *tmp, *red, *gws,
       *qr, *lfb, *svd, *wn;
+  double *Yv2, *Tv2, *lfb2;  // basic pipelined loop: second-parity Q_v, side-stream larfb scratch
   long ldn, ldm, ldb, ldtmp;
   size_t qr_n, lfb_n, svd_n;
   int* meta;  // [0] = carried columns in wn (boosted)
@@ -70,6 +73,9 @@ static size_t plan_rutv(int m, int n, int b, int p_in, RutvWs* w, double* base) 
   v.lfb = take(v.lfb_n);
   v.svd = take(v.svd_n);
   v.meta = (int*)take(8);
+  v.Yv2 = bst ? nullptr : take(ldn * wd);
+  v.Tv2 = bst ? nullptr : take(ldb * wd);
+  v.lfb2 = bst ? nullptr : take(v.lfb_n);
   if (w) *w = v;
   return used / sizeof(double) + 64;
 }
@@ -263,22 +269,23 @@ int randutv_step(int i, int m, int n, int b, int p, int q, bool boosted, Mat T, 
 
 // Side stream for the latency-bound b x b Jacobi SVD (created once, high
 // priority so its few CTAs are dispatched ahead of the GEMM tiles).
-static int side_stream(cudaStream_t* s1, cudaEvent_t* ev) {
-  static cudaStream_t g_s1 = nullptr;
-  static cudaEvent_t g_ev[2];
+static int side_stream(cudaStream_t* s1, cudaEvent_t* ev, cudaStream_t* s2 = nullptr) {
+  static cudaStream_t g_s1 = nullptr, g_s2 = nullptr;
+  static cudaEvent_t g_ev[5];
   static std::once_flag once;
   static int err = 0;
   std::call_once(once, [] {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     if (cudaStreamCreateWithPriority(&g_s1, cudaStreamNonBlocking, hi) != cudaSuccess) err = 1;
-    for (int e = 0; e < 2; ++e)
+    if (cudaStreamCreateWithPriority(&g_s2, cudaStreamNonBlocking, lo) != cudaSuccess) err = 1;
+    for (int e = 0; e < 5; ++e)
       if (cudaEventCreateWithFlags(&g_ev[e], cudaEventDisableTiming) != cudaSuccess) err = 1;
   });
   if (err) return UTV_ERR_CUDA;
   *s1 = g_s1;
-  ev[0] = g_ev[0];
-  ev[1] = g_ev[1];
+  if (s2) *s2 = g_s2;
+  for (int e = 0; e < (s2 ? 5 : 2); ++e) ev[e] = g_ev[e];
   return UTV_OK;
 }
 
@@ -311,49 +318,90 @@ int randutv_basic_range(int i0, int i1, int m, int n, int b, int q, Mat T, Mat U
   if (ws_doubles < plan_rutv(m, n, b, -1, nullptr, nullptr)) return UTV_ERR_WORKSPACE;
   RutvWs w;
   plan_rutv(m, n, b, -1, &w, ws);
-  cudaStream_t s1;
-  cudaEvent_t ev[2];  // [0] R ready (main), [1] SVD done (side)
-  UTV_CHECK(side_stream(&s1, ev));
+  // Streams: st = critical path (sampling, T transforms, panel QRs, rotations);
+  // s1 (high priority) = the b x b Jacobi SVD of step i; s2 = the U and V
+  // right transforms, which only the next rotations read: they fill the SMs
+  // the latency-bound panel QRs leave idle (panels get PBUD CTAs, s2 GEMMs
+  // at most SIDE CTAs, the Jacobi the rest).
+  // ev: [0] R ready (st), [1] SVD done (s1), [2] T right done (st),
+  //     [3] Q_u ready (st), [4] U/V transforms of the pending step done (s2).
+  static const int SIDE = [] {
+    const char* e = getenv("UTV_RU_SIDE");  // tuning knob; 0 = transforms on st
+    return e ? atoi(e) : 88;
+  }();
+  static const int PBUD = [] {
+    const char* e = getenv("UTV_RU_PANEL");
+    return e ? atoi(e) : 48;
+  }();
+  cudaStream_t s1, s2;
+  cudaEvent_t ev[5];
+  UTV_CHECK(side_stream(&s1, ev, &s2));
   const int nsteps = (n + b - 1) / b < i1 ? (n + b - 1) / b : i1;
   long gcol = 0;
-  int pending = -1;  // step whose SVD is in flight on the side stream
+  int pending = -1;  // step whose SVD (and side transforms) are in flight
+  auto finish_pending = [&]() -> int {
+    if (pending < 0) return UTV_OK;
+    UTV_CUDA(cudaStreamWaitEvent(st, ev[1], 0));
+    if (SIDE > 0) UTV_CUDA(cudaStreamWaitEvent(st, ev[4], 0));
+    UTV_CHECK(step_back(pending, pending * b, T, U, V, m, n, n - pending * b, b, errsq, trail2, w, st));
+    pending = -1;
+    return UTV_OK;
+  };
   for (int i = i0; i < nsteps; ++i) {
     const int lo = i * b;
     const int k = m - lo, kc = n - lo;
     if (kc <= b) {
-      if (pending >= 0) {
-        UTV_CUDA(cudaStreamWaitEvent(st, ev[1], 0));
-        UTV_CHECK(step_back(pending, pending * b, T, U, V, m, n, n - pending * b, b, errsq, trail2, w, st));
-        pending = -1;
-      }
+      UTV_CHECK(finish_pending());
       int carried = 0, fin = 0;
       UTV_CHECK(randutv_step(i, m, n, b, 0, q, false, T, U, V, nullptr, ldg, errsq, trail2,
                              svd_status, ws, ws_doubles, &carried, &fin, st));
       break;
     }
     Mat Bk = T.sub(lo, lo, k, kc);
-    Mat Yv{w.Yv, w.ldn, kc, b}, Tv{w.Tv, w.ldb, b, b};
-    // front_a: sampling (randutv.py:185-193) + [Vq, ~] = hqr_full(Y) (:141)
+    const bool alt = SIDE > 0 && (i & 1);  // Q_v double buffer (s2 may still read the other)
+    Mat Yv{alt ? w.Yv2 : w.Yv, w.ldn, kc, b}, Tv{alt ? w.Tv2 : w.Tv, w.ldb, b, b};
+    // sampling (randutv.py:185-193) + [Vq, ~] = hqr_full(Y) (:141)
     UTV_CHECK(sample_basic(Bk, b, q, G + gcol * ldg, ldg, w, st));
     UTV_CHECK(geqrf(Mat{w.Y, w.ldn, kc, b}, Yv, Tv, true, w.qr, w.qr_n, st));
     gcol += k;
-    if (pending >= 0) {
-      UTV_CUDA(cudaStreamWaitEvent(st, ev[1], 0));
-      UTV_CHECK(step_back(pending, pending * b, T, U, V, m, n, n - pending * b, b, errsq, trail2, w, st));
-      pending = -1;
+    UTV_CHECK(finish_pending());
+    Mat Yu{w.Yu, w.ldm, k, b}, Tu{w.Tu, w.ldb, b, b};
+    if (SIDE <= 0) {
+      UTV_CHECK(front_b(lo, T, U, V, Yv, Tv, k, kc, b, w, st));
+    } else {
+      // T right on st (randutv.py:143); V right on s2 (:144); QR of the T panel (:145)
+      UTV_CHECK(larfb('R', false, Yv, Tv, T.sub(0, lo, m, kc), w.lfb, w.lfb_n, st));
+      UTV_CUDA(cudaEventRecord(ev[2], st));
+      UTV_CUDA(cudaStreamWaitEvent(s2, ev[2], 0));
+      gemm_set_max_ctas(SIDE);
+      const int rc = larfb('R', false, Yv, Tv, V.sub(0, lo, n, kc), w.lfb2, w.lfb_n, s2);
+      gemm_set_max_ctas(0);
+      UTV_CHECK(rc);
+      panel_set_max_ctas(PBUD);
+      const int rq = geqrf(T.sub(lo, lo, k, b), Yu, Tu, true, w.qr, w.qr_n, st);
+      panel_set_max_ctas(0);
+      UTV_CHECK(rq);
     }
-    UTV_CHECK(front_b(lo, T, U, V, Yv, Tv, k, kc, b, w, st));
     UTV_CUDA(cudaEventRecord(ev[0], st));
     UTV_CUDA(cudaStreamWaitEvent(s1, ev[0], 0));
     UTV_CHECK(step_svd(lo, T, b, svd_status + i, w, s1));
     UTV_CUDA(cudaEventRecord(ev[1], s1));
     pending = i;
-    UTV_CHECK(front_c(lo, T, U, k, kc, b, w, st));
+    if (SIDE <= 0) {
+      UTV_CHECK(front_c(lo, T, U, k, kc, b, w, st));
+    } else {
+      // U right on s2 (randutv.py:147), T left on st (:148)
+      UTV_CUDA(cudaEventRecord(ev[3], st));
+      UTV_CUDA(cudaStreamWaitEvent(s2, ev[3], 0));
+      gemm_set_max_ctas(SIDE);
+      const int rc = larfb('R', false, Yu, Tu, U.sub(0, lo, m, k), w.lfb2, w.lfb_n, s2);
+      gemm_set_max_ctas(0);
+      UTV_CHECK(rc);
+      UTV_CUDA(cudaEventRecord(ev[4], s2));
+      UTV_CHECK(larfb('L', true, Yu, Tu, T.sub(lo, lo + b, k, kc - b), w.lfb, w.lfb_n, st));
+    }
   }
-  if (pending >= 0) {
-    UTV_CUDA(cudaStreamWaitEvent(st, ev[1], 0));
-    UTV_CHECK(step_back(pending, pending * b, T, U, V, m, n, n - pending * b, b, errsq, trail2, w, st));
-  }
+  UTV_CHECK(finish_pending());
   return UTV_OK;
 }
 

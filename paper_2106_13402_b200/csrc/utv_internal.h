@@ -101,6 +101,8 @@ size_t geqrf_ws_doubles(int rows, int cols, bool want_t);
 // P <- R, Y, T (full cols x cols forward triangle; T must be zero below the diagonal).
 size_t panel_ws_doubles();
 int panel_rows_max();
+// CTA budget for the next full-width panel_qr launches on this host thread (0 = all SMs).
+void panel_set_max_ctas(int n);
 int panel_qr(Mat P, Mat Y, Mat T, const double* fro2, double* ws, cudaStream_t st,
              int max_ctas = 0);
 int geqrf(Mat P, Mat Y, Mat Tw, bool want_t, double* ws, size_t ws_doubles, cudaStream_t st);
