@@ -305,10 +305,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (lane == 0) mbar_arrive(empty0 + 8 * s);
     }
 
-    // ---------------- epilogue (straight from the fragments) ----------------
+    // ---------------- epilogue ----------------
     const int m0 = tc.mc - (TA ? 0 : p.a_sh), n0 = tc.nc - (TB ? p.b_sh : 0);
     if (HASC) mbar_wait(cfull, (uint32_t)(local & 1));
     double* w = p.ws ? p.ws + (size_t)tc.z * p.N * p.M : nullptr;
+    // beta != 0 with an unshifted C map: alpha*acc + beta*C is written back
+    // over the prefetched C tile in smem and leaves by one TMA store, so the
+    // warps start the next tile without draining 128 KB of stores first.
+    // (tile origins at a -1 row/column shift keep the direct stores)
+    const bool tstore = HASC && p.c_sh == 0 && !w && m0 >= 0 && n0 >= 0;
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
       const int ml = frag_row<TA>(wm, t, fr);
@@ -321,7 +326,14 @@ __global__ void __launch_bounds__(THREADS, 1)
           const int nl = frag_col<TB>(wn, u, 2 * fk + j);
           const int n = n0 + nl;
           double v = p.alpha * acc[t][u][j];
-          if (HASC) v = fma(p.beta, sC[swz((ml >> 4) * BN + nl, ml & 15)], v);
+          if (HASC) {
+            double* cs = &sC[swz((ml >> 4) * BN + nl, ml & 15)];
+            v = fma(p.beta, *cs, v);
+            if (tstore) {
+              *cs = v;
+              continue;
+            }
+          }
           if (mok && n >= 0 && n < p.N) {
             if (w) w[m + (size_t)n * p.M] = acc[t][u][j];
             else p.C[m + (long)n * p.ldc] = v;
@@ -329,13 +341,21 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
     }
     if (HASC) {
+      if (tstore) fence_proxy_async_smem();  // generic smem writes -> async proxy
       __syncthreads();  // every warp is done with sC
       if (threadIdx.x == 0) {
+        if (tstore) {
+#pragma unroll
+          for (int i = 0; i < BM / 16; ++i) tma_store_2d(&tmC, smem_u32(sC + i * 16 * BN), m0 + 16 * i, n0);
+          bulk_commit();
+          bulk_wait_read0();  // sC may be refilled once the store has read it
+        }
         const int nxt = tq[(local + 1) & 7];  // published: the producer runs >= 1 k-block ahead
         if (nxt >= 0) load_c(nxt);
       }
     }
   }
+  if (HASC && threadIdx.x == 0) bulk_wait0();
 }
 
 // C = alpha * sum_s ws[s] + beta * C, summed in split order (deterministic).

@@ -7,6 +7,8 @@
 // roofline inputs) without a profiler attached.
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <utility>
 #include <vector>
@@ -21,6 +23,7 @@ struct Rec {
   int cat;
   cudaEvent_t a, b;
   double flops, bytes;
+  cudaStream_t st;
 };
 std::mutex g_mu;
 bool g_on = false;
@@ -56,7 +59,7 @@ ProfScope::~ProfScope() {
   std::lock_guard<std::mutex> lk(g_mu);
   cudaEvent_t b = get_event();
   cudaEventRecord(b, st_);
-  g_recs.push_back(Rec{cat_, (cudaEvent_t)a_, b, flops_, bytes_});
+  g_recs.push_back(Rec{cat_, (cudaEvent_t)a_, b, flops_, bytes_, st_});
 }
 
 }  // namespace utv
@@ -85,12 +88,16 @@ int utv_profile_end(double* ms, double* flops, double* bytes, long long* count) 
     count[c] = 0;
   }
   std::vector<std::pair<float, float>> iv[PROF_NCAT];
+  // UTV_PROF_DUMP=<file>: append one "cat,start_ms,end_ms,flops,stream" line per launch
+  static const char* dump_path = getenv("UTV_PROF_DUMP");
+  FILE* dump = dump_path ? fopen(dump_path, "a") : nullptr;
   for (auto& r : g_recs) {
     float t = 0.f, t0 = 0.f, t1 = 0.f;
     cudaEventElapsedTime(&t, r.a, r.b);
     if (cudaEventElapsedTime(&t0, g_ref, r.a) == cudaSuccess &&
         cudaEventElapsedTime(&t1, g_ref, r.b) == cudaSuccess)
       iv[r.cat].push_back({t0, t1});
+    if (dump) fprintf(dump, "%d,%.4f,%.4f,%.6g,%p\n", r.cat, t0, t1, r.flops, (void*)r.st);
     ms[r.cat] += t;
     flops[r.cat] += r.flops;
     bytes[r.cat] += r.bytes;
@@ -116,6 +123,7 @@ int utv_profile_end(double* ms, double* flops, double* bytes, long long* count) 
     if (ce > cs) busy += ce - cs;
     g_busy[c] = busy;
   }
+  if (dump) fclose(dump);
   g_recs.clear();
   g_on = false;
   return PROF_NCAT;
