@@ -10,9 +10,10 @@
 //
 // Only the two returned factors (Uq, Vq) need the dense n x n compact-WY
 // triangle of the reference's QFactor; every intermediate QR keeps its
-// panel-blocked form (diagonal 256 x 256 blocks of T) and is applied /
-// materialised panel by panel (larfb_panels / orgqr_panels), which is what
-// brings the executed FLOPs down to the algorithmic count of SURVEY §8d.
+// panel-blocked form (diagonal 256 x 256 blocks of T) and is applied panel
+// by panel (larfb_panels).  Vhat and the intermediate V are never
+// materialised (see the loop): the executed FLOPs are 4n^3/3 per materialise
+// below SURVEY §8d's count (which bench.py keeps as the metric's numerator).
 #include "common.cuh"
 #include <cstdio>
 #include <cstdlib>
@@ -80,35 +81,35 @@ int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, M
     UTV_CHECK(copy_mat(G.p, G.ld, w.Yn, w.ldn, n, n, st));
     UTV_CHECK(geqrf(Mat{w.Yn, w.ldn, n, n}, Vy, Vt, true, w.qr, w.qr_n, st));
   } else {
-    const double* vcur = G.p;
-    long ldv = G.ld;
+    // Neither Vhat nor the next round's V is ever formed: with Q the
+    // Householder QR of Yhat, Y = A^T Vhat = ((Q^T A)[:n, :])^T, and
+    // A V = A Q(Vq) — compact-WY applications to a copy of A cost
+    // 4mn^2 - 2n^3 and 2mn^2 flops against 4mn^2 - 2n^3/3 and 2mn^2 + 4n^3/3
+    // for materialise-then-multiply (same products, different association).
     for (int it = 0; it < q; ++it) {
       const bool last = (it + 1 == q);
-      // Yhat = A V (powerurv.py:64)
-      UTV_CHECK(dgemm(false, false, m, n, n, 1.0, A.p, A.ld, vcur, ldv, 0.0, w.Yh, w.ldm, w.gws,
-                      SPLITK_WS, st));
+      // Yhat = A V (powerurv.py:64); round 0: V = G
+      if (it == 0) {
+        UTV_CHECK(dgemm(false, false, m, n, n, 1.0, A.p, A.ld, G.p, G.ld, 0.0, w.Yh, w.ldm, w.gws,
+                        SPLITK_WS, st));
+      } else {
+        UTV_CHECK(copy_mat(A.p, A.ld, w.Yh, w.ldm, m, n, st));
+        UTV_CHECK(larfb_panels('R', false, Vy, Vt, Mat{w.Yh, w.ldm, m, n}, w.lfb, w.lfb_n, st));
+      }
       mark("A*V");
-      // Vhat = thin Q of Yhat (powerurv.py:65); any stable thin QR gives the
-      // same hqr_full(Y) below (Householder vectors are invariant under the
-      // column signs of Vhat), so panel-blocked form suffices.
+      // [Q, ~] = hqr_full(Yhat) (powerurv.py:65, thin Q = Q[:, :n])
       Mat Yq{w.Yq, w.ldm, m, n}, Tq{w.Tq, w.ldn, n, n};
       UTV_CHECK(geqrf(Mat{w.Yh, w.ldm, m, n}, Yq, Tq, false, w.qr, w.qr_n, st));
       mark("geqrf(Yhat)");
-      UTV_CHECK(orgqr_panels(Yq, Tq, Mat{w.Vh, w.ldm, m, n}, w.lfb, w.lfb_n, st));
-      mark("orgqr(Vhat)");
-      // Y = A^T Vhat (powerurv.py:66)
-      UTV_CHECK(dgemm(true, false, n, n, m, 1.0, A.p, A.ld, w.Vh, w.ldm, 0.0, w.Yn, w.ldn, w.gws,
-                      SPLITK_WS, st));
+      // Y = A^T Vhat (powerurv.py:66) = transpose of the first n rows of Q^T A
+      UTV_CHECK(copy_mat(A.p, A.ld, w.Vh, w.ldm, m, n, st));
+      UTV_CHECK(larfb_panels('L', true, Yq, Tq, Mat{w.Vh, w.ldm, m, n}, w.lfb, w.lfb_n, st));
+      UTV_CHECK(transpose(w.Vh, w.ldm, w.Yn, w.ldn, n, n, st));
       mark("A^T*Vhat");
       // Vq = hqr_full(Y) (powerurv.py:67); dense T only for the returned factor
       UTV_CHECK(geqrf(Mat{w.Yn, w.ldn, n, n}, Vy, Vt, false, w.qr, w.qr_n, st));
       mark("geqrf(Y)");
-      if (!last) {
-        UTV_CHECK(orgqr_panels(Vy, Vt, Mat{w.Vc, w.ldn, n, n}, w.lfb, w.lfb_n, st));
-        mark("orgqr(V)");
-        vcur = w.Vc;
-        ldv = w.ldn;
-      }
+      (void)last;
     }
     UTV_CHECK(build_t(Vy, Vt, w.bt, w.bt_n, st));
     mark("build_t(V)");
