@@ -65,6 +65,7 @@ struct Args {
   long ldc;
   double* ws;  // split-K partials [split][N][M] (ld = M)
   int* sched;  // dynamic tile scheduler [ticket, done] (self-resetting), or null = static
+  int tri_a;   // A (N-major, M == K, unshifted) is upper triangular: skip k-blocks below the tile
 };
 
 // Physical double offset inside a 128B-swizzled tile whose 128-byte line is
@@ -140,9 +141,15 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ktot = p.K + p.k_sh;
-  auto nk_of = [&](int z) {
-    const int kb = z * p.k_split;
-    const int ke = min(ktot, kb + p.k_split);
+  // k' range of a tile: its split, clipped below at the tile's first row
+  // when A is upper triangular (A[i, k] = 0 for k < i)
+  auto kbeg_of = [&](const TileCoord& c) {
+    const int kb = c.z * p.k_split;
+    return p.tri_a ? max(kb, (c.mc / BK) * BK) : kb;
+  };
+  auto nk_of = [&](const TileCoord& c) {
+    const int kb = kbeg_of(c);
+    const int ke = min(ktot, c.z * p.k_split + p.k_split);
     return (ke - kb + BK - 1) / BK;
   };
 
@@ -164,13 +171,24 @@ __global__ void __launch_bounds__(THREADS, 1)
   // published before the first TMA (or sentinel arrive) of each tile.
   __shared__ int tq[8];
   int pseq = 0;  // tiles started by the producer
+  // triangular A: a (tile, split) unit entirely left of the tile's first
+  // row has no work and is skipped (the reduce kernel skips it too)
+  auto empty_unit = [&](int t) {
+    if (!p.tri_a) return false;
+    const TileCoord c = tile_of(p, t);
+    return (c.mc / BK) * BK >= min(ktot, (c.z + 1) * p.k_split);
+  };
   auto next_tile = [&](int prev) -> int {
     if (!p.sched) {
-      const int t = prev < 0 ? (int)blockIdx.x : prev + (int)gridDim.x;
+      int t = prev < 0 ? (int)blockIdx.x : prev + (int)gridDim.x;
+      while (t < p.tiles && empty_unit(t)) t += (int)gridDim.x;
       return t < p.tiles ? t : -1;
     }
-    const int t = atomicAdd(p.sched, 1);
-    if (t < p.tiles) return t;
+    while (true) {
+      const int t = atomicAdd(p.sched, 1);
+      if (t >= p.tiles) break;
+      if (!empty_unit(t)) return t;
+    }
     if (atomicAdd(p.sched + 1, 1) == (int)gridDim.x - 1) {
       atomicExch(p.sched, 0);
       atomicExch(p.sched + 1, 0);
@@ -178,7 +196,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     return -1;
   };
   // ---- producer state (thread 0 only) ----
-  int ptile = -1, pit = 0, pnk = 0;
+  int ptile = -1, pit = 0, pnk = 0, pkb = 0;
   long pg = 0;  // global produced k-block count
   TileCoord pc{};
   bool pdone = false;
@@ -186,7 +204,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     ptile = next_tile(-1);
     if (ptile >= 0) {
       pc = tile_of(p, ptile);
-      pnk = nk_of(pc.z);
+      pnk = nk_of(pc);
+      pkb = kbeg_of(pc);
     }
   }
   auto produce_one = [&]() {
@@ -207,7 +226,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t fb = full0 + 8 * s;
     if (pit == 0) tq[(pseq++) & 7] = ptile;
     mbar_arrive_expect_tx(fb, STAGE_BYTES);
-    const int k = pc.z * p.k_split + pit * BK;  // k' (even)
+    const int k = pkb + pit * BK;  // k' (even)
     const uint32_t dA = smem_u32(sA + s * A_ST), dB = smem_u32(sB + s * B_ST);
     if (TA) {
       tma_load_2d(dA, &tmA, fb, k, pc.mc);
@@ -231,7 +250,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       ptile = next_tile(ptile);
       if (ptile >= 0) {
         pc = tile_of(p, ptile);
-        pnk = nk_of(pc.z);
+        pnk = nk_of(pc);
+        pkb = kbeg_of(pc);
       }
     }
   };
@@ -267,7 +287,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int tile = tq[local & 7];
     if (tile < 0) break;
     const TileCoord tc = tile_of(p, tile);
-    const int nk = nk_of(tc.z);
+    const int nk = nk_of(tc);
     double acc[8][4][2];
 #pragma unroll
     for (int t = 0; t < 8; ++t)
@@ -359,14 +379,18 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 // C = alpha * sum_s ws[s] + beta * C, summed in split order (deterministic).
+// tri_ksplit > 0 (triangular A): splits that lie entirely left of a row
+// tile's first k were never computed and are skipped.
 __global__ void splitk_reduce_kernel(const double* __restrict__ ws, int splits, int M, int N,
-                                     double alpha, double beta, double* C, long ldc) {
+                                     double alpha, double beta, double* C, long ldc,
+                                     int tri_ksplit) {
   const size_t total = (size_t)M * N;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
        i += (size_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int z = 0; z < splits; ++z) s += ws[(size_t)z * total + i];
     const int m = (int)(i % M), n = (int)(i / M);
+    const int z0 = tri_ksplit > 0 ? ((m / BM) * BM / BK * BK) / tri_ksplit : 0;
+    double s = 0.0;
+    for (int z = z0; z < splits; ++z) s += ws[(size_t)z * total + i];
     double* c = C + m + (long)n * ldc;
     const double v = alpha * s;
     *c = (beta == 0.0) ? v : fma(beta, *c, v);
@@ -549,6 +573,12 @@ int choose_splits(int tiles, int K) {
 int dgemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, long lda,
           const double* B, long ldb, double beta, double* C, long ldc, double* ws,
           size_t ws_doubles, cudaStream_t st) {
+  return dgemm_ex(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, ws_doubles, st, false);
+}
+
+int dgemm_ex(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, long lda,
+             const double* B, long ldb, double beta, double* C, long ldc, double* ws,
+             size_t ws_doubles, cudaStream_t st, bool tri_a) {
   if (M <= 0 || N <= 0) return UTV_OK;
   UTV_CHECK(get_encode());
   if (K <= 0 || alpha == 0.0) {
@@ -595,6 +625,9 @@ int dgemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, 
 
   const int tm = ceil_div(M + a_sh, gemm::BM), tn = ceil_div(N + b_sh, gemm::BN);
   const int Kp = K + k_sh;
+  // triangular A only in the plain layout (no origin shifts, one split)
+  const bool tri = tri_a && !ta && a_sh == 0 && k_sh == 0 && M == K;
+  // (split-K units left of a row tile's first k are skipped, see empty_unit)
   int splits = choose_splits(tm * tn, Kp);
   if (ws == nullptr) splits = 1;
   while (splits > 1 && (size_t)splits * M * N > ws_doubles) --splits;
@@ -631,11 +664,20 @@ int dgemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, 
   a.C = C; a.ldc = ldc;
   a.ws = use_ws ? ws : nullptr;
   a.sched = gemm_sched_slot(st);
+  a.tri_a = tri ? 1 : 0;
+  double fl = 2.0 * M * N * K;
+  if (tri) {
+    fl = 0.0;
+    for (int t = 0; t < tm; ++t) {
+      const int mc = t * gemm::BM, rows = min(gemm::BM, M - mc);
+      fl += 2.0 * N * rows * (K - (mc / gemm::BK) * gemm::BK);
+    }
+  }
   int cap = num_sms();
   if (g_max_ctas > 0 && g_max_ctas < cap) cap = g_max_ctas;
   const int grid = a.tiles < cap ? a.tiles : cap;
   {
-  ProfScope ps(PROF_GEMM, 2.0 * M * N * K, 8.0 * ((double)M * K + (double)K * N + (beta != 0.0 ? 2.0 : 1.0) * M * N), st);
+  ProfScope ps(PROF_GEMM, fl, 8.0 * ((double)M * K + (double)K * N + (beta != 0.0 ? 2.0 : 1.0) * M * N), st);
   if (hasc) {
     const size_t sm = gemm::Cfg<true>::SMEM;
     if (!ta && !tb) gemm::dgemm_tma_kernel<false, false, true><<<grid, gemm::THREADS, sm, st>>>(mA, mB, mC, a);
@@ -655,7 +697,7 @@ int dgemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, 
     const long total = (long)M * N;
     ProfScope ps(PROF_SPLITK, 0.0, 8.0 * (splits + (beta != 0.0 ? 2 : 1)) * total, st);
     gemm::splitk_reduce_kernel<<<min(8 * num_sms(), ceil_div(total, 256)), 256, 0, st>>>(
-        ws, splits, M, N, alpha, beta, C, ldc);
+        ws, splits, M, N, alpha, beta, C, ldc, tri ? kper : 0);
     UTV_CUDA(cudaGetLastError());
   }
   if (ctmp) UTV_CUDA(cudaFreeAsync(ctmp, st));

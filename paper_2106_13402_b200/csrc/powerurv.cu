@@ -76,6 +76,9 @@ int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, M
     pname[np++] = name;
   };
   mark("start");
+  cudaStream_t sb = nullptr;
+  cudaEvent_t ev_bt0 = nullptr, ev_bt1 = nullptr;
+  bool bt_side = false;
   if (q == 0) {
     // Vq = hqr_full(G) (powerurv.py:58-59); G is read-only -> work on a copy
     UTV_CHECK(copy_mat(G.p, G.ld, w.Yn, w.ldn, n, n, st));
@@ -111,7 +114,29 @@ int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, M
       mark("geqrf(Y)");
       (void)last;
     }
-    UTV_CHECK(build_t(Vy, Vt, w.bt, w.bt_n, st));
+    // Vq's dense triangle is only returned: its off-diagonal blocks are built
+    // on a low-priority side stream (CTA budget) while A Q(Vq) — which reads
+    // only the diagonal blocks — and the final QR run; it fills the SMs the
+    // QR's latency-bound panels leave idle.
+    static const int BT_SIDE = [] {
+      const char* e = getenv("UTV_PURV_BT_SIDE");  // tuning knob; 0 = in stream order
+      return e ? atoi(e) : 64;
+    }();
+    if (BT_SIDE > 0) {
+      UTV_CHECK(aux_stream_low(&sb));
+      UTV_CHECK(aux_event(6, &ev_bt0));
+      UTV_CHECK(aux_event(7, &ev_bt1));
+      UTV_CUDA(cudaEventRecord(ev_bt0, st));
+      UTV_CUDA(cudaStreamWaitEvent(sb, ev_bt0, 0));
+      gemm_set_max_ctas(BT_SIDE);
+      const int rc = build_t(Vy, Vt, w.bt, w.bt_n, sb);
+      gemm_set_max_ctas(0);
+      UTV_CHECK(rc);
+      UTV_CUDA(cudaEventRecord(ev_bt1, sb));
+      bt_side = true;
+    } else {
+      UTV_CHECK(build_t(Vy, Vt, w.bt, w.bt_n, st));
+    }
     mark("build_t(V)");
   }
   // Ahat = A Q(Vq) (powerurv.py:70), formed in R's storage, panel by panel
@@ -121,6 +146,7 @@ int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, M
   // (Uq, R) = hqr_full(Ahat) (powerurv.py:71)
   UTV_CHECK(geqrf(R, Uy, Ut, false, w.qr, w.qr_n, st));
   mark("geqrf(Ahat)");
+  if (bt_side) UTV_CUDA(cudaStreamWaitEvent(st, ev_bt1, 0));  // w.bt reused below
   UTV_CHECK(build_t(Uy, Ut, w.bt, w.bt_n, st));
   mark("build_t(U)");
   if (phases) {

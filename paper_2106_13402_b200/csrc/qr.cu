@@ -95,7 +95,8 @@ static int merge_t(Mat Y, Mat T, int j0, int jb, double* S1, double* S2, double*
   const long lds = round_up(j0, 4);
   UTV_CHECK(dgemm(true, false, j0, jb, rows, 1.0, Y.at(j0, 0), Y.ld, Y.at(j0, j0), Y.ld, 0.0, S1,
                   lds, gws, SPLITK_WS, st));
-  UTV_CHECK(dgemm(false, false, j0, jb, j0, 1.0, T.p, T.ld, S1, lds, 0.0, S2, lds, gws, SPLITK_WS, st));
+  UTV_CHECK(dgemm_ex(false, false, j0, jb, j0, 1.0, T.p, T.ld, S1, lds, 0.0, S2, lds, gws, SPLITK_WS,
+                     st, true));  // T11 upper triangular
   UTV_CHECK(dgemm(false, false, j0, jb, jb, -1.0, S2, lds, T.at(j0, j0), T.ld, 0.0, T.at(0, j0),
                   T.ld, gws, SPLITK_WS, st));
   return UTV_OK;

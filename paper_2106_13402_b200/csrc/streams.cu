@@ -16,6 +16,7 @@ constexpr int NSTREAMS = 4, NEVENTS = 16;
 std::once_flag g_once;
 int g_err = 0;
 cudaStream_t g_streams[NSTREAMS];
+cudaStream_t g_low = nullptr;  // lowest-priority stream for deferred, off-critical-path work
 cudaEvent_t g_events[NEVENTS];
 }  // namespace
 
@@ -25,6 +26,7 @@ static int init_aux() {
     if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) g_err = 1;
     for (int i = 0; i < NSTREAMS; ++i)
       if (cudaStreamCreateWithPriority(&g_streams[i], cudaStreamNonBlocking, hi) != cudaSuccess) g_err = 1;
+    if (cudaStreamCreateWithPriority(&g_low, cudaStreamNonBlocking, lo) != cudaSuccess) g_err = 1;
     for (int i = 0; i < NEVENTS; ++i)
       if (cudaEventCreateWithFlags(&g_events[i], cudaEventDisableTiming) != cudaSuccess) g_err = 1;
   });
@@ -35,6 +37,12 @@ int aux_stream(int idx, cudaStream_t* s) {
   UTV_CHECK(init_aux());
   if (idx < 0 || idx >= NSTREAMS) return UTV_ERR_CUDA;
   *s = g_streams[idx];
+  return UTV_OK;
+}
+
+int aux_stream_low(cudaStream_t* s) {
+  UTV_CHECK(init_aux());
+  *s = g_low;
   return UTV_OK;
 }
 

@@ -15,6 +15,9 @@ int num_sms();
 // events 0-1: randUTV fp64, 2-3: randUTV fp32, 4-5: QR look-ahead.
 int aux_stream(int idx, cudaStream_t* s);
 int aux_event(int idx, cudaEvent_t* e);
+// lowest-priority non-blocking stream (deferred work: powerURV's dense Vq triangle).
+// events 6-7: powerURV side build_t.
+int aux_stream_low(cudaStream_t* s);
 
 // ---- launch accounting / profiling (prof.cu) ----
 enum ProfCat {
@@ -51,6 +54,11 @@ size_t dgemm_ws_doubles(int M, int N, int K);
 int dgemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, long lda,
           const double* B, long ldb, double beta, double* C, long ldc, double* ws,
           size_t ws_doubles, cudaStream_t st);
+// tri_a: A (not transposed, M == K) is upper triangular — the k-blocks below
+// each tile's first row are skipped (TRMM-shaped product at half the flops).
+int dgemm_ex(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, long lda,
+             const double* B, long ldb, double beta, double* C, long ldc, double* ws,
+             size_t ws_doubles, cudaStream_t st, bool tri_a);
 
 // ---- K10 3xTF32 GEMM (gemm_tf32.cu): fp32 operands, ld % 4 == 0, 16B-aligned A/B ----
 int sgemm_tf32x3(bool ta, bool tb, int M, int N, int K, float alpha, const float* A, long lda,
