@@ -91,6 +91,9 @@ SIGNATURES = {
     "utv_profile_begin": (None, []),
     "utv_profile_end": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "utv_profile_busy": (c_int, [c_void_p]),
+    "utv_rng_set_tables": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "utv_rng_pcg64_normals": (c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                      c_void_p, ctypes.c_uint64, c_int, c_void_p]),
 }
 
 PROF_CATEGORIES = ("dgemm_dmma", "splitk_reduce", "panel_qr", "jacobi_rounds",

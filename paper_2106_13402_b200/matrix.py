@@ -23,7 +23,9 @@ class RngStream:
         self._gen = np.random.Generator(np.random.PCG64(self.seed))
 
     def standard_normal(self, m, n):
-        return self._gen.standard_normal((m, n))
+        # large draws: the same stream generated on all host cores (fastrng)
+        from .fastrng import standard_normal
+        return standard_normal(self._gen, (m, n))
 
     def __repr__(self):
         return f"RngStream(seed={self.seed})"

@@ -260,7 +260,8 @@ def _draw_into(rng, k, b, out):
     """rng.standard_normal(k, b) written into out (same draws as the reference)."""
     gen = getattr(rng, "_gen", None)
     if gen is not None:
-        gen.standard_normal((k, b), out=out)
+        from .fastrng import standard_normal_into
+        standard_normal_into(gen, out)
     else:
         out[...] = rng.standard_normal(k, b)
 
