@@ -197,6 +197,13 @@ int utv_powerurv_f64(int m, int n, int q, const double* A, long lda, const doubl
                      double* Uy, long lduy, double* Ut, long ldut, double* R, long ldr,
                      double* Vy, long ldvy, double* Vt, long ldvt, void* work, size_t lwork,
                      void* stream);
+/* Same, plus vq_ready (a cudaEvent_t, may be null): recorded once Vq.Y and
+ * Vq.Twy are final, before A Q(Vq) and the final QR, so the caller can copy
+ * Vq out while the factorisation finishes. */
+int utv_powerurv_f64_ev(int m, int n, int q, const double* A, long lda, const double* G, long ldg,
+                        double* Uy, long lduy, double* Ut, long ldut, double* R, long ldr,
+                        double* Vy, long ldvy, double* Vt, long ldvt, void* work, size_t lwork,
+                        void* stream, void* vq_ready);
 
 /* Instrumentation (no reference counterpart).
  * utv_launch_count: number of libutvb200 kernel launches since load.

@@ -63,6 +63,9 @@ SIGNATURES = {
     "utv_powerurv_f64": (c_int, [c_int, c_int, c_int, c_void_p, c_long, c_void_p, c_long,
                                  c_void_p, c_long, c_void_p, c_long, c_void_p, c_long, c_void_p,
                                  c_long, c_void_p, c_long, c_void_p, c_size_t, c_void_p]),
+    "utv_powerurv_f64_ev": (c_int, [c_int, c_int, c_int, c_void_p, c_long, c_void_p, c_long,
+                                 c_void_p, c_long, c_void_p, c_long, c_void_p, c_long, c_void_p,
+                                 c_long, c_void_p, c_long, c_void_p, c_size_t, c_void_p, c_void_p]),
     "utv_dgeqrf_rows_max": (c_int, []),
     "utv_dgeqp3_bufsize": (c_size_t, [c_int, c_int]),
     "utv_dgeqp3_max_dim": (c_int, []),
@@ -206,18 +209,12 @@ def _ring():
     return _RING, _POOL
 
 
-def d2h_numpy(m):
-    """Contiguous (ld == rows) device block -> new F-order numpy array."""
-    import torch
-    ring, pool = _ring()
-    dt = np.float64 if m.t.dtype == torch.float64 else np.float32
-    out = np.empty((m.rows, m.cols), dtype=dt, order="F")
-    dst = out.reshape(-1, order="F").view(np.uint8)
-    src = m.t.view(-1)[: m.rows * m.cols].view(torch.uint8)
+def _d2h_bytes(src, dst, stream, ring, pool, nthr=8):
+    """Device bytes `src` (torch uint8) -> host bytes `dst` (numpy uint8),
+    staged through the pinned `ring` (DMA on `stream`) with an nthr-way
+    host memcpy per chunk, chunks pipelined against each other."""
     nb = dst.nbytes
-    stream = torch.cuda.current_stream()
     chunks = [(off, min(_RING_CHUNK, nb - off)) for off in range(0, nb, _RING_CHUNK)]
-    nthr = 8
 
     def copy_out(k, off, sz):
         buf = ring[k][0].numpy()
@@ -242,7 +239,77 @@ def d2h_numpy(m):
     for j, o, z in pending:
         ring[j][1].synchronize()
         copy_out(j, o, z)
+
+
+def d2h_numpy(m):
+    """Contiguous (ld == rows) device block -> new F-order numpy array."""
+    import torch
+    ring, pool = _ring()
+    dt = np.float64 if m.t.dtype == torch.float64 else np.float32
+    out = np.empty((m.rows, m.cols), dtype=dt, order="F")
+    dst = out.reshape(-1, order="F").view(np.uint8)
+    src = m.t.view(-1)[m.off: m.off + m.rows * m.cols].view(torch.uint8)
+    _d2h_bytes(src, dst, torch.cuda.current_stream(), ring, pool)
     return out
+
+
+class AsyncD2H:
+    """Background device->host copies of column blocks that are FINAL (no
+    later kernel writes them): each job waits (on the device) for an event
+    of the compute stream, then streams the blocks through a private pinned
+    ring on a private copy stream into preallocated F-order numpy arrays, so
+    results leave the GPU while the factorisation is still running."""
+
+    _shared = {}
+
+    def __init__(self):
+        import queue
+        import threading
+
+        import torch
+        if "ring" not in AsyncD2H._shared:
+            AsyncD2H._shared["ring"] = [(torch.empty(_RING_CHUNK, dtype=torch.uint8, pin_memory=True),
+                                         torch.cuda.Event()) for _ in range(3)]
+        self.ring = AsyncD2H._shared["ring"]
+        _, self.pool = _ring()
+        self.stream = torch.cuda.Stream()
+        self.q = queue.Queue()
+        self.err = None
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
+
+    def push(self, event, blocks):
+        """blocks: list of (DMat with ld == rows, host F-order array, c0, c1)."""
+        self.q.put((event, blocks))
+
+    def _run(self):
+        import torch
+        while True:
+            job = self.q.get()
+            if job is None:
+                return
+            if self.err is not None:
+                continue
+            event, blocks = job
+            try:
+                with torch.cuda.stream(self.stream):
+                    self.stream.wait_event(event)
+                    for m, host, c0, c1 in blocks:
+                        if c1 <= c0:
+                            continue
+                        es = m.esize
+                        src = m.t.view(-1)[m.off + c0 * m.ld: m.off + c1 * m.ld].view(torch.uint8)
+                        dst = host.reshape(-1, order="F")[c0 * m.rows: c1 * m.rows].view(np.uint8)
+                        assert m.ld == m.rows and dst.nbytes == src.numel() and es == host.itemsize
+                        _d2h_bytes(src, dst, self.stream, self.ring, self.pool)
+            except BaseException as e:  # surfaced by finish()
+                self.err = e
+
+    def finish(self):
+        self.q.put(None)
+        self.th.join()
+        if self.err is not None:
+            raise self.err
 
 
 def dempty(rows, cols, ld=None, dtype=None):

@@ -22,7 +22,7 @@ int randutv_basic_f32(int m, int n, int b, int q, float* Tp, long ldt, float* Up
                       int* svd_status, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t powerurv_ws_doubles(int m, int n);
 int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, Mat Vt, double* ws,
-             size_t ws_doubles, cudaStream_t st);
+             size_t ws_doubles, cudaStream_t st, cudaEvent_t vq_ready = nullptr);
 }  // namespace utv
 
 using namespace utv;
@@ -350,6 +350,14 @@ int utv_powerurv_f64(int m, int n, int q, const double* A, long lda, const doubl
                      double* Uy, long lduy, double* Ut, long ldut, double* R, long ldr,
                      double* Vy, long ldvy, double* Vt, long ldvt, void* work, size_t lwork,
                      void* stream) {
+  return utv_powerurv_f64_ev(m, n, q, A, lda, G, ldg, Uy, lduy, Ut, ldut, R, ldr, Vy, ldvy, Vt, ldvt,
+                             work, lwork, stream, nullptr);
+}
+
+int utv_powerurv_f64_ev(int m, int n, int q, const double* A, long lda, const double* G, long ldg,
+                        double* Uy, long lduy, double* Ut, long ldut, double* R, long ldr,
+                        double* Vy, long ldvy, double* Vt, long ldvt, void* work, size_t lwork,
+                        void* stream, void* vq_ready) {
   if (m < 1) return -1;
   if (n < 1 || n > m) return -2;
   if (q < 0) return -3;
@@ -362,7 +370,8 @@ int utv_powerurv_f64(int m, int n, int q, const double* A, long lda, const doubl
   if (!ld_ok(ldvt, n)) return -17;
   return powerurv(m, n, q, Mat{(double*)A, lda, m, n}, Mat{(double*)G, ldg, n, n},
                   Mat{Uy, lduy, m, n}, Mat{Ut, ldut, n, n}, Mat{R, ldr, m, n}, Mat{Vy, ldvy, n, n},
-                  Mat{Vt, ldvt, n, n}, (double*)work, lwork / sizeof(double), S(stream));
+                  Mat{Vt, ldvt, n, n}, (double*)work, lwork / sizeof(double), S(stream),
+                  (cudaEvent_t)vq_ready);
 }
 
 }  // extern "C"

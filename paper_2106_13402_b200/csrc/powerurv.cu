@@ -57,8 +57,10 @@ static size_t plan_purv(int m, int n, PurvWs* w, double* base) {
 
 size_t powerurv_ws_doubles(int m, int n) { return plan_purv(m, n, nullptr, nullptr); }
 
+// vq_ready (optional): recorded once Vq (Y and the dense T) is final, so the
+// caller can start copying it out while A Q(Vq) and the final QR run.
 int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, Mat Vt, double* ws,
-             size_t ws_doubles, cudaStream_t st) {
+             size_t ws_doubles, cudaStream_t st, cudaEvent_t vq_ready) {
   if (m < n) return -1;
   if (q < 0) return -3;
   if (ws_doubles < plan_purv(m, n, nullptr, nullptr)) return UTV_ERR_WORKSPACE;
@@ -83,6 +85,7 @@ int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, M
     // Vq = hqr_full(G) (powerurv.py:58-59); G is read-only -> work on a copy
     UTV_CHECK(copy_mat(G.p, G.ld, w.Yn, w.ldn, n, n, st));
     UTV_CHECK(geqrf(Mat{w.Yn, w.ldn, n, n}, Vy, Vt, true, w.qr, w.qr_n, st));
+    if (vq_ready) UTV_CUDA(cudaEventRecord(vq_ready, st));
   } else {
     // Neither Vhat nor the next round's V is ever formed: with Q the
     // Householder QR of Yhat, Y = A^T Vhat = ((Q^T A)[:n, :])^T, and
@@ -133,9 +136,11 @@ int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, M
       gemm_set_max_ctas(0);
       UTV_CHECK(rc);
       UTV_CUDA(cudaEventRecord(ev_bt1, sb));
+      if (vq_ready) UTV_CUDA(cudaEventRecord(vq_ready, sb));
       bt_side = true;
     } else {
       UTV_CHECK(build_t(Vy, Vt, w.bt, w.bt_n, st));
+      if (vq_ready) UTV_CUDA(cudaEventRecord(vq_ready, st));
     }
     mark("build_t(V)");
   }

@@ -206,12 +206,17 @@ class PowerUrvRun:
         self.Vy = dempty(n, n)
         self.Vt = dempty(n, n)
 
-    def run(self, A: DMat, G: DMat):
+    def run(self, A: DMat, G: DMat, vq_event=None):
+        """vq_event (torch.cuda.Event, optional): recorded once Vq is final."""
         lib = load()
-        check(lib.utv_powerurv_f64(
+        ev = None
+        if vq_event is not None:
+            vq_event.record()          # materialises the CUDA event; re-recorded inside
+            ev = vq_event.cuda_event
+        check(lib.utv_powerurv_f64_ev(
             self.m, self.n, self.q, A.ptr, A.ld, G.ptr, G.ld, self.Uy.ptr, self.Uy.ld, self.Ut.ptr,
             self.Ut.ld, self.R.ptr, self.R.ld, self.Vy.ptr, self.Vy.ld, self.Vt.ptr, self.Vt.ld,
-            self.ws.data_ptr(), self.lw, stream_ptr()), "utv_powerurv_f64")
+            self.ws.data_ptr(), self.lw, stream_ptr(), ev), "utv_powerurv_f64")
 
 
 # ---------------------------------------------------------------------------

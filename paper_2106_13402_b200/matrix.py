@@ -31,16 +31,26 @@ class RngStream:
         return f"RngStream(seed={self.seed})"
 
 
-def check_matrix(a, name="matrix"):
-    """float64 cast, 2-D, positive dims, all finite (matrix.py:36-49)."""
+def check_matrix(a, name="matrix", finite=True):
+    """float64 cast, 2-D, positive dims, all finite (matrix.py:36-49).
+
+    finite=False skips the host scan: callers that upload the matrix anyway
+    run the same check on the device (raise_if_nonfinite) before any draw."""
     a = np.asarray(a, dtype=np.float64)
     if a.ndim != 2:
         raise DimensionError(f"{name} must be 2-D, got shape {a.shape}")
     if a.shape[0] < 1 or a.shape[1] < 1:
         raise DimensionError(f"{name} must have positive dimensions, got {a.shape}")
-    if not np.isfinite(a).all():
+    if finite and not np.isfinite(a).all():
         raise ValueError(f"{name} contains NaN or Inf entries")
     return a
+
+
+def raise_if_nonfinite(d, name="matrix"):
+    """The finite half of check_matrix, on a device copy (DMat)."""
+    import torch
+    if not bool(torch.isfinite(d.tensor()).all()):
+        raise ValueError(f"{name} contains NaN or Inf entries")
 
 
 def gaussian(m, n, rng):

@@ -18,7 +18,7 @@ import numpy as np
 from . import device as dv
 from ._lib import deye, dfrom_numpy
 from .errors import ConsistencyError, ConvergenceError, DimensionError
-from .matrix import check_matrix, frobenius_norm
+from .matrix import raise_if_nonfinite, check_matrix, frobenius_norm
 
 
 @dataclass
@@ -78,8 +78,8 @@ class UtvFactorization:
         return min(self.steps_done * self.b, self.T.shape[1])
 
 
-def _validate(a, b, q, p):
-    a = check_matrix(a)
+def _validate(a, b, q, p, finite=True):
+    a = check_matrix(a, finite=finite)
     m, n = a.shape
     if m < n:
         raise DimensionError(f"randutv needs m >= n, got {a.shape}; factor the transpose")
@@ -139,11 +139,11 @@ def randutv_basic(a, b, q, rng, record_trailing=False, *, dtype=np.float64):
     m, n and b must then be multiples of 4.  The default float64 path is the
     reference-exact drop-in."""
     import torch
-    a = _validate(a, b, q, 0)
+    f32 = np.dtype(dtype) == np.float32
+    a = _validate(a, b, q, 0, finite=f32)   # fp64: the finite scan runs on the device copy
     m, n = a.shape
     b = int(b)
     q = int(q)
-    f32 = np.dtype(dtype) == np.float32
     if f32 and (m % 4 or n % 4 or b % 4):
         raise ValueError("the fp32 variant needs m, n and b to be multiples of 4")
     if not f32:
@@ -160,12 +160,12 @@ def randutv_basic(a, b, q, rng, record_trailing=False, *, dtype=np.float64):
     return _finish_basic(a, b, q, run, t_dev, U, V, record_trailing, f32)
 
 
-def _finish_basic(a, b, q, run, t_dev, U, V, record_trailing, f32):
+def _finish_basic(a, b, q, run, t_dev, U, V, record_trailing, f32, host=None, anorm=None):
     status = run.status.cpu().numpy()
     if (status < 0).any():
         raise ConvergenceError("b x b Jacobi SVD failed to converge")
     masses = run.errsq.cpu().numpy()
-    tracker = ErrorTracker.start(frobenius_norm(a))
+    tracker = ErrorTracker.start(frobenius_norm(a) if anorm is None else anorm)
     if f32:
         tracker.neg_tol = 1e-5
     for mass in masses:
@@ -174,9 +174,13 @@ def _finish_basic(a, b, q, run, t_dev, U, V, record_trailing, f32):
     if record_trailing:
         trailing = [float(math.sqrt(max(x, 0.0))) for x in run.trail2.cpu().numpy()]
         trailing[-1] = 0.0
+    if host is not None:
+        u_h, t_h, v_h = host
+    else:
+        u_h, t_h, v_h = U.to_numpy(), t_dev.to_numpy(), V.to_numpy()
     return UtvFactorization(
-        U=np.asfortranarray(U.to_numpy()), T=np.asfortranarray(t_dev.to_numpy()),
-        V=np.asfortranarray(V.to_numpy()), b=b, steps_done=run.steps, oversample=0, power=q,
+        U=np.asfortranarray(u_h), T=np.asfortranarray(t_h),
+        V=np.asfortranarray(v_h), b=b, steps_done=run.steps, oversample=0, power=q,
         errors=list(tracker.history), trailing_fro=trailing)
 
 
@@ -281,6 +285,8 @@ def _randutv_basic_pipelined(a, b, q, rng, record_trailing):
     sizes = [m - i * b for i in range(max(0, steps - 1))]       # rows of each drawn block
     offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64) if sizes else np.zeros(1, np.int64)
     t_dev = dfrom_numpy(a)
+    raise_if_nonfinite(t_dev)                               # before any draw, as the reference
+    anorm = math.sqrt(float(dv.sumsq(t_dev).item()))        # ErrorTracker's ||A||_F (matrix.py:79-81)
     run = dv.RandUtvRun(m, n, b, q, record_trailing)
     U, V = deye(m), deye(n)
     G = _lib.dempty(b, max(int(offs[-1]), 1))               # block i = columns offs[i]:offs[i+1]
@@ -294,6 +300,15 @@ def _randutv_basic_pipelined(a, b, q, rng, record_trailing):
     ring = _pinned_pair(8 * b * max(int(maxcols), 1))
     copy_stream = torch.cuda.Stream()
     comp = torch.cuda.current_stream()
+    # results leave the GPU while later steps run: after steps [j0, j1) the
+    # columns < j1*b of T, U and V are final (later steps only touch columns
+    # >= lo, randutv.py:143-156)
+    contiguous = t_dev.ld == m and U.ld == m and V.ld == n
+    out = None
+    if contiguous:
+        out = (np.empty((m, m), order="F"), np.empty((m, n), order="F"), np.empty((n, n), order="F"))
+        d2h = _lib.AsyncD2H()
+        done_cols = 0
     for gi, (j0, j1) in enumerate(groups):
         d0, d1 = min(j0, len(sizes)), min(j1, len(sizes))
         ncol = int(offs[d1] - offs[d0])
@@ -314,7 +329,18 @@ def _randutv_basic_pipelined(a, b, q, rng, record_trailing):
             run.errsq.data_ptr(), run.trail2.data_ptr() if run.trail2 is not None else None,
             run.status.data_ptr(), run.ws.data_ptr(), run.lw, _lib.stream_ptr()),
             "utv_randutv_basic_steps_f64")
-    return _finish_basic(a, b, q, run, t_dev, U, V, record_trailing, False)
+        if contiguous:
+            fin = min(n, j1 * b) if j1 < steps else n
+            if fin > done_cols:
+                ev = torch.cuda.Event()
+                ev.record(comp)
+                blocks = [(U, out[0], done_cols, fin if j1 < steps else m), (t_dev, out[1], done_cols, fin),
+                          (V, out[2], done_cols, fin)]
+                d2h.push(ev, blocks)
+                done_cols = fin
+    if contiguous:
+        d2h.finish()
+    return _finish_basic(a, b, q, run, t_dev, U, V, record_trailing, False, host=out, anorm=anorm)
 
 
 def randutv_boosted(a, b, q, p, rng, record_trailing=False):
