@@ -153,13 +153,30 @@ static int row_grid(long rows) {
 
 size_t lu_ws_doubles() { return SPLITK_WS; }
 
-// In-place LU without pivoting of (P - diag(s)) for a rows x n panel (rows >= n):
-// L (unit lower trapezoidal) below the diagonal, U' on/above, s[0..n) = signs.
-int getrf_signed(Mat P, double* s, double* ws, size_t ws_doubles, cudaStream_t st) {
-  const int rows = P.rows, n = P.cols;
-  if (rows < n) return -1;
-  for (int j0 = 0; j0 < n; j0 += lu::NB) {
-    const int jb = n - j0 < lu::NB ? n - j0 : lu::NB;
+// B[:, j1:c1) -= B[:, j0:j1) M[j0:j1, j1:c1),  M = op(A) upper.
+static int trsm_update(bool trans, const double* A, long lda, Mat B, int j0, int j1, int c1,
+                       double* ws, size_t ws_doubles, cudaStream_t st) {
+  const int m = B.rows;
+  if (!trans)
+    return dgemm(false, false, m, c1 - j1, j1 - j0, -1.0, B.at(0, j0), B.ld,
+                 A + j0 + (long)j1 * lda, lda, 1.0, B.at(0, j1), B.ld, ws, ws_doubles, st);
+  // M[j0.., j1..] = A[j1.., j0..]^T
+  return dgemm(false, true, m, c1 - j1, j1 - j0, -1.0, B.at(0, j0), B.ld,
+               A + j1 + (long)j0 * lda, lda, 1.0, B.at(0, j1), B.ld, ws, ws_doubles, st);
+}
+
+// Outer block width of the two-level LU / trsm: the NB-wide kernels and
+// K = NB updates stay inside one NB2-wide column panel (HBM-bound but narrow),
+// the wide trailing updates are K = NB2 DMMA GEMMs (tensor-bound).
+constexpr int NB2 = 256;
+
+// In-place LU without pivoting of (P - diag(s)) for the columns [c0, c1) of a
+// rows x n panel, rows [c0, rows), updating only columns < c1 (NB blocks).
+static int getrf_signed_cols(Mat P, int c0, int c1, double* s, double* ws, size_t ws_doubles,
+                             cudaStream_t st) {
+  const int rows = P.rows;
+  for (int j0 = c0; j0 < c1; j0 += lu::NB) {
+    const int jb = c1 - j0 < lu::NB ? c1 - j0 : lu::NB;
     {
       ProfScope ps(PROF_OPS, 2.0 / 3.0 * jb * jb * jb, 16.0 * jb * jb, st);
       lu::lu_diag_kernel<<<1, lu::THREADS, 0, st>>>(P.p, P.ld, j0, jb, s);
@@ -173,30 +190,56 @@ int getrf_signed(Mat P, double* s, double* ws, size_t ws_doubles, cudaStream_t s
       lu::lu_panel_kernel<<<row_grid(rows - j0 - jb), lu::THREADS, 0, st>>>(a);
       UTV_CUDA(cudaGetLastError());
     }
-    if (j0 + jb < n) {
+    if (j0 + jb < c1) {
       {
-        ProfScope ps(PROF_OPS, (double)jb * jb * (n - j0 - jb), 16.0 * jb * (n - j0 - jb), st);
-        lu::lu_u12_kernel<<<ceil_div(n - j0 - jb, lu::THREADS), lu::THREADS, 0, st>>>(
-            P.p, P.ld, j0, jb, j0 + jb, n);
+        ProfScope ps(PROF_OPS, (double)jb * jb * (c1 - j0 - jb), 16.0 * jb * (c1 - j0 - jb), st);
+        lu::lu_u12_kernel<<<ceil_div(c1 - j0 - jb, lu::THREADS), lu::THREADS, 0, st>>>(
+            P.p, P.ld, j0, jb, j0 + jb, c1);
         UTV_CUDA(cudaGetLastError());
       }
-      // A22 -= L21 U12
-      UTV_CHECK(dgemm(false, false, rows - j0 - jb, n - j0 - jb, jb, -1.0, P.at(j0 + jb, j0), P.ld,
+      // A22 -= L21 U12 inside the panel
+      UTV_CHECK(dgemm(false, false, rows - j0 - jb, c1 - j0 - jb, jb, -1.0, P.at(j0 + jb, j0), P.ld,
                       P.at(j0, j0 + jb), P.ld, 1.0, P.at(j0 + jb, j0 + jb), P.ld, ws, ws_doubles, st));
     }
   }
   return UTV_OK;
 }
 
-// B (m x n) <- B * M^{-1}, M = op(A) upper triangular n x n:
-// uplo 'U' + trans 'N' (M = A) or uplo 'L' + trans 'T' (M = A^T); unit diagonal optional.
-int trsm_right_upper(bool trans, bool unit, int n, const double* A, long lda, Mat B, double* ws,
-                     size_t ws_doubles, cudaStream_t st) {
+// In-place LU without pivoting of (P - diag(s)) for a rows x n panel (rows >= n):
+// L (unit lower trapezoidal) below the diagonal, U' on/above, s[0..n) = signs.
+// Right-looking over NB2-wide panels: panel LU (NB blocks), U12 = L11^{-1} A12
+// by NB-block forward substitution, A22 -= L21 U12 as one K = NB2 GEMM.
+int getrf_signed(Mat P, double* s, double* ws, size_t ws_doubles, cudaStream_t st) {
+  const int rows = P.rows, n = P.cols;
+  if (rows < n) return -1;
+  for (int J0 = 0; J0 < n; J0 += NB2) {
+    const int J1 = n - J0 < NB2 ? n : J0 + NB2;
+    UTV_CHECK(getrf_signed_cols(P, J0, J1, s, ws, ws_doubles, st));
+    if (J1 >= n) break;
+    for (int j0 = J0; j0 < J1; j0 += lu::NB) {
+      const int jb = J1 - j0 < lu::NB ? J1 - j0 : lu::NB;
+      {
+        ProfScope ps(PROF_OPS, (double)jb * jb * (n - J1), 16.0 * jb * (n - J1), st);
+        lu::lu_u12_kernel<<<ceil_div(n - J1, lu::THREADS), lu::THREADS, 0, st>>>(P.p, P.ld, j0, jb,
+                                                                                  J1, n);
+        UTV_CUDA(cudaGetLastError());
+      }
+      if (j0 + jb < J1)
+        UTV_CHECK(dgemm(false, false, J1 - j0 - jb, n - J1, jb, -1.0, P.at(j0 + jb, j0), P.ld,
+                        P.at(j0, J1), P.ld, 1.0, P.at(j0 + jb, J1), P.ld, ws, ws_doubles, st));
+    }
+    UTV_CHECK(dgemm(false, false, rows - J1, n - J1, J1 - J0, -1.0, P.at(J1, J0), P.ld,
+                    P.at(J0, J1), P.ld, 1.0, P.at(J1, J1), P.ld, ws, ws_doubles, st));
+  }
+  return UTV_OK;
+}
+
+// B[:, c0:c1) <- B[:, c0:c1) M[c0:c1, c0:c1]^{-1} (NB blocks, updates inside the panel).
+static int trsm_cols(bool trans, bool unit, const double* A, long lda, Mat B, int c0, int c1,
+                     double* ws, size_t ws_doubles, cudaStream_t st) {
   const int m = B.rows;
-  if (B.cols != n) return -1;
-  if (m <= 0 || n <= 0) return UTV_OK;
-  for (int j0 = 0; j0 < n; j0 += lu::NB) {
-    const int jb = n - j0 < lu::NB ? n - j0 : lu::NB;
+  for (int j0 = c0; j0 < c1; j0 += lu::NB) {
+    const int jb = c1 - j0 < lu::NB ? c1 - j0 : lu::NB;
     lu::PanelArgs a;
     a.P = B.p; a.ldp = B.ld; a.rbeg = 0; a.rows = m; a.j0 = j0; a.jb = jb;
     a.A = A; a.lda = lda; a.trans = trans ? 1 : 0; a.unit = unit ? 1 : 0;
@@ -205,17 +248,24 @@ int trsm_right_upper(bool trans, bool unit, int n, const double* A, long lda, Ma
       lu::lu_panel_kernel<<<row_grid(m), lu::THREADS, 0, st>>>(a);
       UTV_CUDA(cudaGetLastError());
     }
-    if (j0 + jb < n) {
-      // B[:, j0+jb:] -= X_j M[j0:j0+jb, j0+jb:]
-      if (!trans)
-        UTV_CHECK(dgemm(false, false, m, n - j0 - jb, jb, -1.0, B.at(0, j0), B.ld,
-                        A + j0 + (long)(j0 + jb) * lda, lda, 1.0, B.at(0, j0 + jb), B.ld, ws,
-                        ws_doubles, st));
-      else  // M[j0.., j0+jb..] = A[j0+jb.., j0..]^T
-        UTV_CHECK(dgemm(false, true, m, n - j0 - jb, jb, -1.0, B.at(0, j0), B.ld,
-                        A + (j0 + jb) + (long)j0 * lda, lda, 1.0, B.at(0, j0 + jb), B.ld, ws,
-                        ws_doubles, st));
-    }
+    if (j0 + jb < c1) UTV_CHECK(trsm_update(trans, A, lda, B, j0, j0 + jb, c1, ws, ws_doubles, st));
+  }
+  return UTV_OK;
+}
+
+// B (m x n) <- B * M^{-1}, M = op(A) upper triangular n x n:
+// uplo 'U' + trans 'N' (M = A) or uplo 'L' + trans 'T' (M = A^T); unit diagonal optional.
+// Two levels like getrf_signed: NB2-wide panels solved in NB blocks, then
+// B[:, J1:] -= X_J M[J0:J1, J1:] as one K = NB2 GEMM.
+int trsm_right_upper(bool trans, bool unit, int n, const double* A, long lda, Mat B, double* ws,
+                     size_t ws_doubles, cudaStream_t st) {
+  const int m = B.rows;
+  if (B.cols != n) return -1;
+  if (m <= 0 || n <= 0) return UTV_OK;
+  for (int J0 = 0; J0 < n; J0 += NB2) {
+    const int J1 = n - J0 < NB2 ? n : J0 + NB2;
+    UTV_CHECK(trsm_cols(trans, unit, A, lda, B, J0, J1, ws, ws_doubles, st));
+    if (J1 < n) UTV_CHECK(trsm_update(trans, A, lda, B, J0, J1, n, ws, ws_doubles, st));
   }
   return UTV_OK;
 }

@@ -276,19 +276,32 @@ def tsqr(x, comm, ops, chunk_rows=None):
         e_i = ops.eye(n)
     # ---- back down the local tree ----
     if nch > 1:
-        f = ops.zeros(nch * n, n)
-        ops.lacpy(e_i, ops.sub(f, 0, 0, n, n))
-        ops.larfb("L", False, ys, ts, f)
+        f = ops.empty(nch * n, n)
+        q_times_top(ys, ts, e_i, f, ops)
         tops = [ops.sub(f, c * n, 0, n, n) for c in range(nch)]
     else:
         tops = [e_i]
-    q = ops.zeros(m, n)
+    q = ops.empty(m, n)
     for c, (r0, nr) in enumerate(chunks):
-        qc = ops.sub(q, r0, 0, nr, n)
-        ops.lacpy(tops[c], ops.sub(qc, 0, 0, n, n))
         y, t = leaves[c]
-        ops.larfb("L", False, y, t, qc)
+        q_times_top(y, t, tops[c], ops.sub(q, r0, 0, nr, n), ops)
     return q, r
+
+
+def q_times_top(y, t, top, out, ops):
+    """out = Q [top; 0] for Q = I - Y T Y^T (y: k x n unit lower, t: the full
+    n x n forward triangle, top: n x n).  The zero block below top is never
+    touched: W = T (Y1^T top) costs 2 n^3 each, then out = [top; 0] - Y W is
+    one k x n x n product — half the flops of a dense larfb on [top; 0]."""
+    k, n = ops.shape(y)
+    y1 = ops.sub(y, 0, 0, n, n)
+    w = ops.gemm("N", "N", 1.0, t, ops.gemm("T", "N", 1.0, y1, top))
+    o1 = ops.sub(out, 0, 0, n, n)
+    ops.lacpy(top, o1)
+    ops.gemm("N", "N", -1.0, y1, w, 1.0, o1)
+    if k > n:
+        ops.gemm("N", "N", -1.0, ops.sub(y, n, 0, k - n, n), w, 0.0, ops.sub(out, n, 0, k - n, n))
+    return out
 
 
 def householder_from_q(q, r_in, comm, ops):
@@ -359,8 +372,9 @@ def power_urv_sharded(a_loc, g, q, comm=None, ops=None, chunk_rows=None):
             vy, vt = ops.geqrf(y)                                    # :67
             if it + 1 < q:
                 v = ops.orgqr(vy, vt, n)                             # :68
-    ahat = ops.copy(a_loc)                                           # :70
-    ops.larfb("R", False, vy, vt, ahat)
+    # :70 A Q(Vq): V explicit (n x n, 2n^3) and one m_i x n x n product, not
+    # a compact-WY apply to a copy of A (>= 4 m_i n^2 for n reflectors)
+    ahat = ops.gemm("N", "N", 1.0, a_loc, ops.orgqr(vy, vt, n))
     qh, r_in = tsqr(ahat, comm, ops, chunk_rows)                     # :71
     del ahat
     uy, ut, r, _ = householder_from_q(qh, r_in, comm, ops)

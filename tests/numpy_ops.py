@@ -39,7 +39,7 @@ class NumpyOps:
         r = alpha * ((a.T if ta == "T" else a) @ (b.T if tb == "T" else b))
         if c is None:
             return np.asfortranarray(r)
-        c[...] = r + beta * c
+        c[...] = r if beta == 0.0 else r + beta * c
         return c
 
     def geqrf(self, a):
