@@ -122,9 +122,9 @@ static int geqrf_blocked(Mat P, Mat Y, Mat T, bool want_t, const double* fro2, A
   cudaEvent_t ev_narrow = nullptr, ev_panel = nullptr;
   const bool lookahead = cols > blk;
   if (lookahead) {
-    UTV_CHECK(aux_stream(1, &sa));
-    UTV_CHECK(aux_event(4, &ev_narrow));
-    UTV_CHECK(aux_event(5, &ev_panel));
+    UTV_CHECK(aux_stream_for(st, 1, &sa));
+    UTV_CHECK(aux_event_for(st, 4, &ev_narrow));
+    UTV_CHECK(aux_event_for(st, 5, &ev_panel));
   }
   static const int LA_CTAS = [] {
     const char* e = getenv("UTV_LA_CTAS");  // tuning knob (default 48)

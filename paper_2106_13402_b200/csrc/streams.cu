@@ -46,6 +46,66 @@ int aux_stream_low(cudaStream_t* s) {
   return UTV_OK;
 }
 
+// Per-caller-stream sets of look-ahead streams/events: two factorisations
+// issued on different caller streams (e.g. independent TSQR leaves) must
+// not share a side stream, or their latency-bound panels serialise.  The
+// null key is the global set above.
+namespace {
+constexpr int NKEYS = 8;
+struct AuxSet {
+  cudaStream_t key;
+  cudaStream_t streams[NSTREAMS];
+  cudaEvent_t events[NEVENTS];
+};
+std::mutex g_keys_mu;
+AuxSet g_keys[NKEYS];
+int g_nkeys = 0;
+}  // namespace
+
+static int aux_set(cudaStream_t key, AuxSet** out) {
+  UTV_CHECK(init_aux());
+  std::lock_guard<std::mutex> lk(g_keys_mu);
+  for (int i = 0; i < g_nkeys; ++i)
+    if (g_keys[i].key == key) {
+      *out = &g_keys[i];
+      return UTV_OK;
+    }
+  if (g_nkeys == NKEYS) return UTV_ERR_CUDA;
+  AuxSet& a = g_keys[g_nkeys];
+  int lo = 0, hi = 0;
+  if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return UTV_ERR_CUDA;
+  for (int i = 0; i < NSTREAMS; ++i)
+    if (cudaStreamCreateWithPriority(&a.streams[i], cudaStreamNonBlocking, hi) != cudaSuccess)
+      return UTV_ERR_CUDA;
+  for (int i = 0; i < NEVENTS; ++i)
+    if (cudaEventCreateWithFlags(&a.events[i], cudaEventDisableTiming) != cudaSuccess)
+      return UTV_ERR_CUDA;
+  a.key = key;
+  ++g_nkeys;
+  *out = &a;
+  return UTV_OK;
+}
+
+int aux_stream_for(cudaStream_t key, int idx, cudaStream_t* s) {
+  if (key == nullptr || key == cudaStreamLegacy || key == cudaStreamPerThread) return aux_stream(idx, s);
+  if (idx < 0 || idx >= NSTREAMS) return UTV_ERR_CUDA;
+  AuxSet* a = nullptr;
+  const int rc = aux_set(key, &a);
+  if (rc != UTV_OK) return aux_stream(idx, s);  // table full: fall back to the shared set
+  *s = a->streams[idx];
+  return UTV_OK;
+}
+
+int aux_event_for(cudaStream_t key, int idx, cudaEvent_t* e) {
+  if (key == nullptr || key == cudaStreamLegacy || key == cudaStreamPerThread) return aux_event(idx, e);
+  if (idx < 0 || idx >= NEVENTS) return UTV_ERR_CUDA;
+  AuxSet* a = nullptr;
+  const int rc = aux_set(key, &a);
+  if (rc != UTV_OK) return aux_event(idx, e);
+  *e = a->events[idx];
+  return UTV_OK;
+}
+
 int aux_event(int idx, cudaEvent_t* e) {
   UTV_CHECK(init_aux());
   if (idx < 0 || idx >= NEVENTS) return UTV_ERR_CUDA;

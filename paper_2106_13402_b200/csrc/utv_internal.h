@@ -15,6 +15,9 @@ int num_sms();
 // events 0-1: randUTV fp64, 2-3: randUTV fp32, 4-5: QR look-ahead.
 int aux_stream(int idx, cudaStream_t* s);
 int aux_event(int idx, cudaEvent_t* e);
+// the same, private to the caller's stream `key` (a set per distinct key)
+int aux_stream_for(cudaStream_t key, int idx, cudaStream_t* s);
+int aux_event_for(cudaStream_t key, int idx, cudaEvent_t* e);
 // lowest-priority non-blocking stream (deferred work: powerURV's dense Vq triangle).
 // events 6-7: powerURV side build_t.
 int aux_stream_low(cudaStream_t* s);

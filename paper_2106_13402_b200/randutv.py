@@ -308,6 +308,7 @@ def _randutv_basic_pipelined(a, b, q, rng, record_trailing):
     if contiguous:
         out = (np.empty((m, m), order="F"), np.empty((m, n), order="F"), np.empty((n, n), order="F"))
         d2h = _lib.AsyncD2H()
+        d2h.prefault(list(out))
         done_cols = 0
     for gi, (j0, j1) in enumerate(groups):
         d0, d1 = min(j0, len(sizes)), min(j1, len(sizes))
