@@ -331,13 +331,22 @@ def run_ours(args):
         a_host = A.to_numpy()
         a_host = np.asfortranarray(a_host)
         del T, U, V
-        torch.cuda.empty_cache()
+
+        def e2e_step():
+            fr = pk.randutv_basic(a_host, b, q, pk.RngStream(3))
+            fp = pk.power_urv(a_host, q, pk.RngStream(2))
+            del fr, fp
+
+        # one untimed call (pinned rings, host thread pools, device buffers
+        # in the caching allocator), then E2E_STEPS timed calls, wall clock
+        e2e_step()
         torch.cuda.synchronize()
+        e2e_steps = max(1, min(args.steps, 2))
         te = time.perf_counter()
-        fr = pk.randutv_basic(a_host, b, q, pk.RngStream(3))
-        fp = pk.power_urv(a_host, q, pk.RngStream(2))
+        for _ in range(e2e_steps):
+            e2e_step()
         torch.cuda.synchronize()
-        e2e_s = time.perf_counter() - te
+        e2e_s = (time.perf_counter() - te) / e2e_steps
         if ws > 1:
             tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
@@ -346,9 +355,9 @@ def run_ours(args):
         d2h = 8 * (3 * n * n + 5 * n * n) + 8 * (-(-n // b)) * 2
         e2e = {"value": ws * flops / e2e_s / 1e12, "unit": "TFLOP/s", "seconds": e2e_s,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "steps": e2e_steps, "warmup": 1,
                "includes": "host PCG64 draws of G (reference RNG), H2D of A and G, device "
                            "factorisations, D2H of U,T,V and Uq,R,Vq (numpy results)"}
-        del fr, fp
 
     g = prof["dgemm_dmma"]
     # GEMM flops over the union of GEMM launch intervals (all streams): the

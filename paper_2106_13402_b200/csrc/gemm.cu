@@ -675,6 +675,11 @@ int dgemm_ex(bool ta, bool tb, int M, int N, int K, double alpha, const double* 
   }
   int cap = num_sms();
   if (g_max_ctas > 0 && g_max_ctas < cap) cap = g_max_ctas;
+  static const int env_cap = [] {  // debug knob: grid cap of every GEMM (0 = off)
+    const char* e = getenv("UTV_GEMM_CTAS");
+    return e ? atoi(e) : 0;
+  }();
+  if (env_cap > 0 && env_cap < cap) cap = env_cap;
   const int grid = a.tiles < cap ? a.tiles : cap;
   {
   ProfScope ps(PROF_GEMM, fl, 8.0 * ((double)M * K + (double)K * N + (beta != 0.0 ? 2.0 : 1.0) * M * N), st);
