@@ -22,7 +22,8 @@ int randutv_basic_f32(int m, int n, int b, int q, float* Tp, long ldt, float* Up
                       int* svd_status, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t powerurv_ws_doubles(int m, int n);
 int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, Mat Vt, double* ws,
-             size_t ws_doubles, cudaStream_t st, cudaEvent_t vq_ready = nullptr);
+             size_t ws_doubles, cudaStream_t st, cudaEvent_t vq_ready, const double* yhat0 = nullptr,
+             long ldy0 = 0);
 }  // namespace utv
 
 using namespace utv;
@@ -372,6 +373,27 @@ int utv_powerurv_f64_ev(int m, int n, int q, const double* A, long lda, const do
                   Mat{Uy, lduy, m, n}, Mat{Ut, ldut, n, n}, Mat{R, ldr, m, n}, Mat{Vy, ldvy, n, n},
                   Mat{Vt, ldvt, n, n}, (double*)work, lwork / sizeof(double), S(stream),
                   (cudaEvent_t)vq_ready);
+}
+
+int utv_powerurv_f64_yhat(int m, int n, int q, const double* A, long lda, const double* Yhat0,
+                          long ldy0, double* Uy, long lduy, double* Ut, long ldut, double* R,
+                          long ldr, double* Vy, long ldvy, double* Vt, long ldvt, void* work,
+                          size_t lwork, void* stream, void* vq_ready) {
+  if (m < 1) return -1;
+  if (n < 1 || n > m) return -2;
+  if (q < 1) return -3;
+  if (!ld_ok(lda, m)) return -5;
+  if (Yhat0 == nullptr) return -6;
+  if (!ld_ok(ldy0, m)) return -7;
+  if (!ld_ok(lduy, m)) return -9;
+  if (!ld_ok(ldut, n)) return -11;
+  if (!ld_ok(ldr, m)) return -13;
+  if (!ld_ok(ldvy, n)) return -15;
+  if (!ld_ok(ldvt, n)) return -17;
+  return powerurv(m, n, q, Mat{(double*)A, lda, m, n}, Mat{nullptr, n, n, n},
+                  Mat{Uy, lduy, m, n}, Mat{Ut, ldut, n, n}, Mat{R, ldr, m, n}, Mat{Vy, ldvy, n, n},
+                  Mat{Vt, ldvt, n, n}, (double*)work, lwork / sizeof(double), S(stream),
+                  (cudaEvent_t)vq_ready, Yhat0, ldy0);
 }
 
 }  // extern "C"

@@ -59,8 +59,12 @@ size_t powerurv_ws_doubles(int m, int n) { return plan_purv(m, n, nullptr, nullp
 
 // vq_ready (optional): recorded once Vq (Y and the dense T) is final, so the
 // caller can start copying it out while A Q(Vq) and the final QR run.
+// yhat0 (optional, q >= 1): the caller already formed Yhat = A G (e.g. as
+// K-chunked products while G was still being drawn on the host); G is then
+// not read.
 int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, Mat Vt, double* ws,
-             size_t ws_doubles, cudaStream_t st, cudaEvent_t vq_ready) {
+             size_t ws_doubles, cudaStream_t st, cudaEvent_t vq_ready, const double* yhat0,
+             long ldy0) {
   if (m < n) return -1;
   if (q < 0) return -3;
   if (ws_doubles < plan_purv(m, n, nullptr, nullptr)) return UTV_ERR_WORKSPACE;
@@ -95,7 +99,9 @@ int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, M
     for (int it = 0; it < q; ++it) {
       const bool last = (it + 1 == q);
       // Yhat = A V (powerurv.py:64); round 0: V = G
-      if (it == 0) {
+      if (it == 0 && yhat0) {
+        UTV_CHECK(copy_mat(yhat0, ldy0, w.Yh, w.ldm, m, n, st));
+      } else if (it == 0) {
         UTV_CHECK(dgemm(false, false, m, n, n, 1.0, A.p, A.ld, G.p, G.ld, 0.0, w.Yh, w.ldm, w.gws,
                         SPLITK_WS, st));
       } else {

@@ -219,6 +219,19 @@ class PowerUrvRun:
             self.ws.data_ptr(), self.lw, stream_ptr(), ev), "utv_powerurv_f64")
 
 
+    def run_yhat(self, A: DMat, Yhat0: DMat, vq_event=None):
+        """q >= 1 with the first product Yhat = A G already formed (utv_powerurv_f64_yhat)."""
+        lib = load()
+        ev = None
+        if vq_event is not None:
+            vq_event.record()
+            ev = vq_event.cuda_event
+        check(lib.utv_powerurv_f64_yhat(
+            self.m, self.n, self.q, A.ptr, A.ld, Yhat0.ptr, Yhat0.ld, self.Uy.ptr, self.Uy.ld,
+            self.Ut.ptr, self.Ut.ld, self.R.ptr, self.R.ld, self.Vy.ptr, self.Vy.ld, self.Vt.ptr,
+            self.Vt.ld, self.ws.data_ptr(), self.lw, stream_ptr(), ev), "utv_powerurv_f64_yhat")
+
+
 # ---------------------------------------------------------------------------
 # TSQR / Householder-reconstruction building blocks (row-sharded powerURV)
 # ---------------------------------------------------------------------------

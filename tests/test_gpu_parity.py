@@ -113,6 +113,27 @@ def test_power_urv_c2_shape_small_against_oracle():
     assert np.abs(f.Uq.Y - ref["Uy"]).max() < 1e-8
 
 
+@pytest.mark.parametrize("m,n,q", [(2304, 2048, 1), (2048, 2048, 2), (2600, 2100, 1)])
+def test_power_urv_streamed_draw_matches_from_sample(m, n, q):
+    """power_urv at n >= 2048 draws G row block by row block while the device
+    forms Yhat = A G as K-chunked GEMMs (utv_powerurv_f64_yhat): the same G as
+    the reference's single n x n draw (identical generator state afterwards)
+    and the same factorisation as power_urv_from_sample on that G."""
+    import paper_2106_13402_b200 as pk
+    rng_a = np.random.default_rng(m + n + q)
+    a = np.asfortranarray(rng_a.standard_normal((m, n)) * np.exp(-np.arange(n) / (n / 8.0)))
+    r1, r2 = pk.RngStream(9), pk.RngStream(9)
+    f = pk.power_urv(a, q, r1)
+    g = pk.gaussian(n, n, r2)
+    ref = pk.power_urv_from_sample(a, q, g)
+    assert r1._gen.bit_generator.state == r2._gen.bit_generator.state
+    anorm2 = np.linalg.norm(a, 2)
+    assert _mixed_ok(np.diag(f.R), np.diag(ref.R), anorm2)
+    assert np.abs(f.Vq.Y - ref.Vq.Y).max() < 1e-8
+    assert np.abs(f.Uq.Y - ref.Uq.Y).max() < 1e-8
+    assert np.abs(f.Vq.Twy - ref.Vq.Twy).max() < 1e-8
+
+
 def test_api_errors_match_reference():
     import paper_2106_13402_b200 as pk
     with pytest.raises(pk.DimensionError):
