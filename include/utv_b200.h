@@ -197,13 +197,14 @@ int utv_powerurv_f64(int m, int n, int q, const double* A, long lda, const doubl
                      double* Uy, long lduy, double* Ut, long ldut, double* R, long ldr,
                      double* Vy, long ldvy, double* Vt, long ldvt, void* work, size_t lwork,
                      void* stream);
-/* Same, plus vq_ready (a cudaEvent_t, may be null): recorded once Vq.Y and
- * Vq.Twy are final, before A Q(Vq) and the final QR, so the caller can copy
- * Vq out while the factorisation finishes. */
+/* Same, plus two cudaEvent_t (each may be null): vq_ready is recorded once
+ * Vq.Y and Vq.Twy are final, before A Q(Vq) and the final QR; r_ready once
+ * R and Uq.Y are final, before Uq's dense triangle is built — so the caller
+ * can copy results out while the factorisation finishes. */
 int utv_powerurv_f64_ev(int m, int n, int q, const double* A, long lda, const double* G, long ldg,
                         double* Uy, long lduy, double* Ut, long ldut, double* R, long ldr,
                         double* Vy, long ldvy, double* Vt, long ldvt, void* work, size_t lwork,
-                        void* stream, void* vq_ready);
+                        void* stream, void* vq_ready, void* r_ready);
 /* Same with q >= 1 and the first power-round product Yhat = A G supplied by
  * the caller (m x n, device, read only) instead of G: the public power_urv
  * forms it as K-chunked products while G is still being drawn on the host
@@ -212,7 +213,7 @@ int utv_powerurv_f64_ev(int m, int n, int q, const double* A, long lda, const do
 int utv_powerurv_f64_yhat(int m, int n, int q, const double* A, long lda, const double* Yhat0,
                           long ldy0, double* Uy, long lduy, double* Ut, long ldut, double* R,
                           long ldr, double* Vy, long ldvy, double* Vt, long ldvt, void* work,
-                          size_t lwork, void* stream, void* vq_ready);
+                          size_t lwork, void* stream, void* vq_ready, void* r_ready);
 
 /* Instrumentation (no reference counterpart).
  * utv_launch_count: number of libutvb200 kernel launches since load.

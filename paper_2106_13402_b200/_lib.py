@@ -65,11 +65,12 @@ SIGNATURES = {
                                  c_long, c_void_p, c_long, c_void_p, c_size_t, c_void_p]),
     "utv_powerurv_f64_ev": (c_int, [c_int, c_int, c_int, c_void_p, c_long, c_void_p, c_long,
                                  c_void_p, c_long, c_void_p, c_long, c_void_p, c_long, c_void_p,
-                                 c_long, c_void_p, c_long, c_void_p, c_size_t, c_void_p, c_void_p]),
+                                 c_long, c_void_p, c_long, c_void_p, c_size_t, c_void_p, c_void_p,
+                                 c_void_p]),
     "utv_powerurv_f64_yhat": (c_int, [c_int, c_int, c_int, c_void_p, c_long, c_void_p, c_long,
                                    c_void_p, c_long, c_void_p, c_long, c_void_p, c_long, c_void_p,
                                    c_long, c_void_p, c_long, c_void_p, c_size_t, c_void_p,
-                                   c_void_p]),
+                                   c_void_p, c_void_p]),
     "utv_dgeqrf_rows_max": (c_int, []),
     "utv_dgeqp3_bufsize": (c_size_t, [c_int, c_int]),
     "utv_dgeqp3_max_dim": (c_int, []),

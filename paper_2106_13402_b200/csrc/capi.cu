@@ -23,7 +23,7 @@ int randutv_basic_f32(int m, int n, int b, int q, float* Tp, long ldt, float* Up
 size_t powerurv_ws_doubles(int m, int n);
 int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, Mat Vt, double* ws,
              size_t ws_doubles, cudaStream_t st, cudaEvent_t vq_ready, const double* yhat0 = nullptr,
-             long ldy0 = 0);
+             long ldy0 = 0, cudaEvent_t r_ready = nullptr);
 }  // namespace utv
 
 using namespace utv;
@@ -352,13 +352,13 @@ int utv_powerurv_f64(int m, int n, int q, const double* A, long lda, const doubl
                      double* Vy, long ldvy, double* Vt, long ldvt, void* work, size_t lwork,
                      void* stream) {
   return utv_powerurv_f64_ev(m, n, q, A, lda, G, ldg, Uy, lduy, Ut, ldut, R, ldr, Vy, ldvy, Vt, ldvt,
-                             work, lwork, stream, nullptr);
+                             work, lwork, stream, nullptr, nullptr);
 }
 
 int utv_powerurv_f64_ev(int m, int n, int q, const double* A, long lda, const double* G, long ldg,
                         double* Uy, long lduy, double* Ut, long ldut, double* R, long ldr,
                         double* Vy, long ldvy, double* Vt, long ldvt, void* work, size_t lwork,
-                        void* stream, void* vq_ready) {
+                        void* stream, void* vq_ready, void* r_ready) {
   if (m < 1) return -1;
   if (n < 1 || n > m) return -2;
   if (q < 0) return -3;
@@ -372,13 +372,13 @@ int utv_powerurv_f64_ev(int m, int n, int q, const double* A, long lda, const do
   return powerurv(m, n, q, Mat{(double*)A, lda, m, n}, Mat{(double*)G, ldg, n, n},
                   Mat{Uy, lduy, m, n}, Mat{Ut, ldut, n, n}, Mat{R, ldr, m, n}, Mat{Vy, ldvy, n, n},
                   Mat{Vt, ldvt, n, n}, (double*)work, lwork / sizeof(double), S(stream),
-                  (cudaEvent_t)vq_ready);
+                  (cudaEvent_t)vq_ready, nullptr, 0, (cudaEvent_t)r_ready);
 }
 
 int utv_powerurv_f64_yhat(int m, int n, int q, const double* A, long lda, const double* Yhat0,
                           long ldy0, double* Uy, long lduy, double* Ut, long ldut, double* R,
                           long ldr, double* Vy, long ldvy, double* Vt, long ldvt, void* work,
-                          size_t lwork, void* stream, void* vq_ready) {
+                          size_t lwork, void* stream, void* vq_ready, void* r_ready) {
   if (m < 1) return -1;
   if (n < 1 || n > m) return -2;
   if (q < 1) return -3;
@@ -393,7 +393,7 @@ int utv_powerurv_f64_yhat(int m, int n, int q, const double* A, long lda, const 
   return powerurv(m, n, q, Mat{(double*)A, lda, m, n}, Mat{nullptr, n, n, n},
                   Mat{Uy, lduy, m, n}, Mat{Ut, ldut, n, n}, Mat{R, ldr, m, n}, Mat{Vy, ldvy, n, n},
                   Mat{Vt, ldvt, n, n}, (double*)work, lwork / sizeof(double), S(stream),
-                  (cudaEvent_t)vq_ready, Yhat0, ldy0);
+                  (cudaEvent_t)vq_ready, Yhat0, ldy0, (cudaEvent_t)r_ready);
 }
 
 }  // extern "C"

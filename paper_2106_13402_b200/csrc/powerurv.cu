@@ -59,12 +59,14 @@ size_t powerurv_ws_doubles(int m, int n) { return plan_purv(m, n, nullptr, nullp
 
 // vq_ready (optional): recorded once Vq (Y and the dense T) is final, so the
 // caller can start copying it out while A Q(Vq) and the final QR run.
+// r_ready (optional): recorded once R and Uq.Y are final (before Uq's dense
+// triangle is built), so the caller can start copying them out.
 // yhat0 (optional, q >= 1): the caller already formed Yhat = A G (e.g. as
 // K-chunked products while G was still being drawn on the host); G is then
 // not read.
 int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, Mat Vt, double* ws,
              size_t ws_doubles, cudaStream_t st, cudaEvent_t vq_ready, const double* yhat0,
-             long ldy0) {
+             long ldy0, cudaEvent_t r_ready) {
   if (m < n) return -1;
   if (q < 0) return -3;
   if (ws_doubles < plan_purv(m, n, nullptr, nullptr)) return UTV_ERR_WORKSPACE;
@@ -157,6 +159,7 @@ int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, M
   // (Uq, R) = hqr_full(Ahat) (powerurv.py:71)
   UTV_CHECK(geqrf(R, Uy, Ut, false, w.qr, w.qr_n, st));
   mark("geqrf(Ahat)");
+  if (r_ready) UTV_CUDA(cudaEventRecord(r_ready, st));  // R and Uq.Y are final; Uq.Twy follows
   if (bt_side) UTV_CUDA(cudaStreamWaitEvent(st, ev_bt1, 0));  // w.bt reused below
   UTV_CHECK(build_t(Uy, Ut, w.bt, w.bt_n, st));
   mark("build_t(U)");

@@ -206,30 +206,31 @@ class PowerUrvRun:
         self.Vy = dempty(n, n)
         self.Vt = dempty(n, n)
 
-    def run(self, A: DMat, G: DMat, vq_event=None):
-        """vq_event (torch.cuda.Event, optional): recorded once Vq is final."""
+    @staticmethod
+    def _ev(e):
+        if e is None:
+            return None
+        e.record()                     # materialises the CUDA event; re-recorded inside
+        return e.cuda_event
+
+    def run(self, A: DMat, G: DMat, vq_event=None, r_event=None):
+        """vq_event / r_event (torch.cuda.Event, optional): recorded once Vq,
+        resp. R and Uq.Y, are final."""
         lib = load()
-        ev = None
-        if vq_event is not None:
-            vq_event.record()          # materialises the CUDA event; re-recorded inside
-            ev = vq_event.cuda_event
         check(lib.utv_powerurv_f64_ev(
             self.m, self.n, self.q, A.ptr, A.ld, G.ptr, G.ld, self.Uy.ptr, self.Uy.ld, self.Ut.ptr,
             self.Ut.ld, self.R.ptr, self.R.ld, self.Vy.ptr, self.Vy.ld, self.Vt.ptr, self.Vt.ld,
-            self.ws.data_ptr(), self.lw, stream_ptr(), ev), "utv_powerurv_f64")
+            self.ws.data_ptr(), self.lw, stream_ptr(), self._ev(vq_event), self._ev(r_event)),
+            "utv_powerurv_f64")
 
-
-    def run_yhat(self, A: DMat, Yhat0: DMat, vq_event=None):
+    def run_yhat(self, A: DMat, Yhat0: DMat, vq_event=None, r_event=None):
         """q >= 1 with the first product Yhat = A G already formed (utv_powerurv_f64_yhat)."""
         lib = load()
-        ev = None
-        if vq_event is not None:
-            vq_event.record()
-            ev = vq_event.cuda_event
         check(lib.utv_powerurv_f64_yhat(
             self.m, self.n, self.q, A.ptr, A.ld, Yhat0.ptr, Yhat0.ld, self.Uy.ptr, self.Uy.ld,
             self.Ut.ptr, self.Ut.ld, self.R.ptr, self.R.ld, self.Vy.ptr, self.Vy.ld, self.Vt.ptr,
-            self.Vt.ld, self.ws.data_ptr(), self.lw, stream_ptr(), ev), "utv_powerurv_f64_yhat")
+            self.Vt.ld, self.ws.data_ptr(), self.lw, stream_ptr(), self._ev(vq_event),
+            self._ev(r_event)), "utv_powerurv_f64_yhat")
 
 
 # ---------------------------------------------------------------------------
