@@ -9,8 +9,20 @@ import torch
 import paper_2106_13402_b200.device as dv
 from paper_2106_13402_b200 import _lib
 from paper_2106_13402_b200._lib import dempty, deye
-A = dempty(n, n); A.t.normal_()
-if what == "geqrf":
+if what == "rutv32":
+    import bench
+    A = bench.make_rank_deficient_f32(n, 2000, 50)
+else:
+    A = dempty(n, n); A.t.normal_()
+if what == "rutv32":
+    b = 512; steps = -(-n // b)
+    G = dempty(b, sum(n - i * b for i in range(steps - 1)), dtype=torch.float32); G.t.normal_()
+    run = dv.RandUtvRun32(n, n, b, 2)
+    T = dempty(n, n, dtype=torch.float32); U = dempty(n, n, dtype=torch.float32); V = dempty(n, n, dtype=torch.float32)
+    def f():
+        T.t.copy_(A.t); U.t.zero_(); U.t[:, :n].fill_diagonal_(1.0); V.t.zero_(); V.t[:, :n].fill_diagonal_(1.0)
+        run.run(T, U, V, G)
+elif what == "geqrf":
     B = dempty(n, n)
     def f(): B.t.copy_(A.t); dv.geqrf(B)
 elif what == "purv":
@@ -44,3 +56,7 @@ for k, v in prof.items():
 per_stream = collections.defaultdict(float)
 for s, e, c, st in ev: per_stream[st] += e - s
 for st, v in per_stream.items(): print(f"  stream {st}: {v:.2f} ms of launches")
+# per stream and category
+psc = collections.defaultdict(float)
+for s_, e_, c_, st_ in ev: psc[(st_, names[c_])] += e_ - s_
+for (st_, c_), v in sorted(psc.items()): print(f"    {st_} {c_:14s} {v:9.2f} ms")
