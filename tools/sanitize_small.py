@@ -31,5 +31,16 @@ if what in ("all", "purv"):
     pk.power_urv(a, 2, pk.RngStream(2))
     from paper_2106_13402_b200.sharded import Comm, power_urv_sharded
     power_urv_sharded(dfrom_numpy(a), dfrom_numpy(orc.draw_gaussian(orc.gaussian_stream(1), 96, 96)), 1, Comm(), chunk_rows=140)
+if what in ("all", "lu"):
+    q0, _ = np.linalg.qr(rng.standard_normal((900, 600)))
+    dv.getrf_signed(dfrom_numpy(q0))
+    t = np.eye(600) + rng.standard_normal((600, 600)) * 0.01
+    for uplo, trans, diag in (("U", "N", "N"), ("L", "T", "U")):
+        dv.trsm_right(uplo, trans, diag, dfrom_numpy(t), dfrom_numpy(rng.standard_normal((500, 600))))
+if what in ("all", "purv_stream"):
+    import paper_2106_13402_b200.powerurv as pu
+    pu.STREAM_MIN_N = 64
+    a, _ = orc.decay_matrix(200, 1e-5, seed=5, m=260)
+    pk.power_urv(a, 1, pk.RngStream(3))
 torch.cuda.synchronize()
 print("done", what)
