@@ -47,7 +47,8 @@ constexpr uint32_t TILE_BYTES = BM * BK * 4;  // 16 KB (A or B, raw or hi or lo)
 constexpr uint32_t RAW_BYTES = 2 * TILE_BYTES;
 constexpr uint32_t CONV_BYTES = 4 * TILE_BYTES;  // hiA loA hiB loB
 constexpr size_t SMEM = (size_t)RAW_STAGES * RAW_BYTES + (size_t)CONV_STAGES * CONV_BYTES + 1024 + 512;
-constexpr uint32_t TMEM_COLS = ACC_STAGES * BN;  // 256
+constexpr uint32_t SUM_COL = ACC_STAGES * BN;   // running chunk sum (128 columns) after the buffers
+constexpr uint32_t TMEM_COLS = 512;              // 2 x 128 accumulator + 128 running sum, pow2
 
 struct Args {
   int M, N, K;
@@ -110,6 +111,19 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+      ::"r"(taddr), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+        "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+        "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+        "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+        "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+        "r"(__float_as_uint(v[15]))
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
 __device__ __forceinline__ float rna_tf32(float x) {
@@ -335,13 +349,18 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ================= epilogue =================
     // 16 warps: lane quarter q = warp & 3 (TMEM lanes 32q..32q+31), column
     // slice h = (warp - EPI_WARP0) >> 2 (EPI_COLS columns).  Chunk
-    // accumulators are summed in registers with round-to-nearest adds, then
-    // written once per tile.
+    // accumulators are summed with round-to-nearest adds into a running sum
+    // kept in TMEM (columns SUM_COL..), 16 columns at a time — no thread
+    // holds a whole row slice in registers (the 896-thread block leaves 72
+    // registers per thread) — and each accumulator buffer is released as
+    // soon as it has been folded in; the tile then goes from the running sum
+    // to C.
     const int q = warp & 3, h = (warp - EPI_WARP0) >> 2;
     const int nchunk = (nk + CHUNK_KB - 1) / CHUNK_KB;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const uint32_t saddr = tmem_base + lane_off + SUM_COL + h * EPI_COLS;
     long ch = 0;
     for (int local = 0;; ++local) {
-      float acc[EPI_COLS];
       int tile = 0;
       for (int cc = 0; cc < nchunk; ++cc, ++ch) {
         const int as = (int)(ch % ACC_STAGES);
@@ -351,13 +370,18 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (tile < 0) break;
         }
         fence_after_sync();
-        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + h * EPI_COLS;
+        const uint32_t taddr = tmem_base + lane_off + as * BN + h * EPI_COLS;
 #pragma unroll
         for (int c0 = 0; c0 < EPI_COLS; c0 += 16) {
           float v[16];
           tmem_ld16(taddr + c0, v);
+          if (cc > 0) {
+            float sum[16];
+            tmem_ld16(saddr + c0, sum);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) acc[c0 + j] = (cc == 0) ? v[j] : acc[c0 + j] + v[j];
+            for (int j = 0; j < 16; ++j) v[j] = sum[j] + v[j];
+          }
+          tmem_st16(saddr + c0, v);
         }
         fence_before_sync();
         __syncwarp();
@@ -366,23 +390,28 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (tile < 0) break;
       const int mc = (tile % p.tm) * BM, nc = (tile / p.tm) * BN + h * EPI_COLS;
       const int m = mc + q * 32 + lane;
-      if (m < p.M) {
 #pragma unroll
-        for (int c0 = 0; c0 < EPI_COLS; c0 += 16) {
-          float cv[16];
-          if (p.beta != 0.0f) {
+      for (int c0 = 0; c0 < EPI_COLS; c0 += 16) {
+        float v[16];
+        tmem_ld16(saddr + c0, v);  // warp-collective: outside the row guard
+        if (m < p.M) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const int n = nc + c0 + j;
-              cv[j] = (n < p.N) ? p.C[m + (long)n * p.ldc] : 0.0f;
+          for (int j0 = 0; j0 < 16; j0 += 8) {
+            float cv[8];
+            if (p.beta != 0.0f) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const int n = nc + c0 + j0 + j;
+                cv[j] = (n < p.N) ? p.C[m + (long)n * p.ldc] : 0.0f;
+              }
             }
-          }
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int n = nc + c0 + j;
-            if (n < p.N) {
-              const float r = p.alpha * acc[c0 + j];
-              p.C[m + (long)n * p.ldc] = (p.beta == 0.0f) ? r : fmaf(p.beta, cv[j], r);
+            for (int j = 0; j < 8; ++j) {
+              const int n = nc + c0 + j0 + j;
+              if (n < p.N) {
+                const float r = p.alpha * v[j0 + j];
+                p.C[m + (long)n * p.ldc] = (p.beta == 0.0f) ? r : fmaf(p.beta, cv[j], r);
+              }
             }
           }
         }
