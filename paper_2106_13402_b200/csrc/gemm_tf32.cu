@@ -48,7 +48,8 @@ constexpr uint32_t RAW_BYTES = 2 * TILE_BYTES;
 constexpr uint32_t CONV_BYTES = 4 * TILE_BYTES;  // hiA loA hiB loB
 constexpr size_t SMEM = (size_t)RAW_STAGES * RAW_BYTES + (size_t)CONV_STAGES * CONV_BYTES + 1024 + 512;
 constexpr uint32_t SUM_COL = ACC_STAGES * BN;   // running chunk sum (128 columns) after the buffers
-constexpr uint32_t TMEM_COLS = 512;              // 2 x 128 accumulator + 128 running sum, pow2
+constexpr uint32_t A_COL = SUM_COL + BN;         // A operand hi|lo per conversion stage (2 x 64 columns)
+constexpr uint32_t TMEM_COLS = 512;              // 2 x 128 accumulator + 128 running sum + 128 A
 
 struct Args {
   int M, N, K;
@@ -86,6 +87,15 @@ __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t da, uint64_t
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
       "l"(da), "l"(db), "r"(idesc_tf32()), "r"(accum));
+}
+
+// A from TMEM (M = 128 lanes x 8 tf32 columns), B from shared memory.
+__device__ __forceinline__ void umma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc_tf32()), "r"(accum));
 }
 
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
@@ -260,15 +270,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (lane == 0) {
           const uint32_t tmem_d = tmem_base + as * BN;
           const uint32_t base = smem_u32(conv + c * CONV_BYTES);
-          const uint32_t hiA = base, loA = base + TILE_BYTES, hiB = base + 2 * TILE_BYTES,
-                         loB = base + 3 * TILE_BYTES;
+          const uint32_t hiB = base + 2 * TILE_BYTES, loB = base + 3 * TILE_BYTES;
+          const uint32_t hiA = tmem_base + A_COL + c * 2 * BK, loA = hiA + BK;  // TMEM columns
 #pragma unroll
           for (int ks = 0; ks < BK / 8; ++ks) {
-            const uint32_t off = ks * 32;  // 8 tf32 = 32 bytes along K
+            const uint32_t off = ks * 32;  // 8 tf32 = 32 bytes along K (B in smem)
             const uint32_t acc0 = (!chunk_start || ks > 0) ? 1u : 0u;
-            umma_tf32(tmem_d, kmajor_sw128_desc(loA + off), kmajor_sw128_desc(hiB + off), acc0);
-            umma_tf32(tmem_d, kmajor_sw128_desc(hiA + off), kmajor_sw128_desc(loB + off), 1u);
-            umma_tf32(tmem_d, kmajor_sw128_desc(hiA + off), kmajor_sw128_desc(hiB + off), 1u);
+            umma_tf32_ts(tmem_d, loA + ks * 8, kmajor_sw128_desc(hiB + off), acc0);
+            umma_tf32_ts(tmem_d, hiA + ks * 8, kmajor_sw128_desc(loB + off), 1u);
+            umma_tf32_ts(tmem_d, hiA + ks * 8, kmajor_sw128_desc(hiB + off), 1u);
           }
           umma_commit(conv_empty + 8 * c);
           if (chunk_end) {
@@ -305,26 +315,50 @@ __global__ void __launch_bounds__(THREADS, 1)
         const float* rA = (const float*)(raw + s * RAW_BYTES);
         const float* rB = rA + BM * BK;
         float* cb = (float*)(conv + c * CONV_BYTES);
-        // 2 operands x 128 rows x 8 quads = 2048 quads, 8 per thread
+        // ---- A: row m = 32 (warp & 3) + lane, k half kh, straight to TMEM
+        //      (tcgen05.st: a warp reaches only its lane quarter) ----
+        {
+          const int cw = warp - CONV_WARP0, kh = cw >> 2, m = 32 * (warp & 3) + lane;
+          float hv[16], lv[16];
 #pragma unroll
-        for (int it = 0; it < 8; ++it) {
+          for (int j = 0; j < 16; j += 4) {
+            const int k = kh * 16 + j;
+            float4 x;
+            if (TA) {  // K-major raw tile, 128B-swizzled by the TMA
+              x = *(const float4*)(rA + m * BK + (((k >> 2) ^ (m & 7)) << 2));
+            } else {   // MN-major raw tile: consecutive lanes read consecutive rows
+              x.x = rA[(k + 0) * BM + m];
+              x.y = rA[(k + 1) * BM + m];
+              x.z = rA[(k + 2) * BM + m];
+              x.w = rA[(k + 3) * BM + m];
+            }
+            hv[j + 0] = rna_tf32(x.x); lv[j + 0] = x.x - hv[j + 0];
+            hv[j + 1] = rna_tf32(x.y); lv[j + 1] = x.y - hv[j + 1];
+            hv[j + 2] = rna_tf32(x.z); lv[j + 2] = x.z - hv[j + 2];
+            hv[j + 3] = rna_tf32(x.w); lv[j + 3] = x.w - hv[j + 3];
+          }
+          const uint32_t ta = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + A_COL + c * 2 * BK + kh * 16;
+          tmem_st16(ta, hv);
+          tmem_st16(ta + BK, lv);
+        }
+        // ---- B: 128 rows x 8 quads = 1024 quads, 4 per thread, K-major SW128 smem ----
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
           const int idx = it * 256 + ct;
-          const int opnd = idx >> 10;          // 0 = A, 1 = B
-          const bool kmaj = opnd == 0 ? TA : !TB;
+          const bool kmaj = !TB;
           // K-major raw rows are 128 B: 8 consecutive threads read one row
           // (conflict-free float4); MN-major raw: consecutive threads take
           // consecutive rows (conflict-free scalar columns)
-          const int r = kmaj ? ((idx >> 3) & 127) : (idx & 127);  // row (m or n)
+          const int r = kmaj ? ((idx >> 3) & 127) : (idx & 127);  // row (n)
           const int qd = kmaj ? (idx & 7) : ((idx >> 7) & 7);       // k quad
-          const float* src = opnd == 0 ? rA : rB;
           float4 x;
           if (kmaj) {
-            x = *(const float4*)(src + r * BK + qd * 4);
+            x = *(const float4*)(rB + r * BK + qd * 4);
           } else {
-            x.x = src[(qd * 4 + 0) * BM + r];
-            x.y = src[(qd * 4 + 1) * BM + r];
-            x.z = src[(qd * 4 + 2) * BM + r];
-            x.w = src[(qd * 4 + 3) * BM + r];
+            x.x = rB[(qd * 4 + 0) * BM + r];
+            x.y = rB[(qd * 4 + 1) * BM + r];
+            x.z = rB[(qd * 4 + 2) * BM + r];
+            x.w = rB[(qd * 4 + 3) * BM + r];
           }
           float4 h, l;
           h.x = rna_tf32(x.x); l.x = x.x - h.x;
@@ -332,11 +366,12 @@ __global__ void __launch_bounds__(THREADS, 1)
           h.z = rna_tf32(x.z); l.z = x.z - h.z;
           h.w = rna_tf32(x.w); l.w = x.w - h.w;
           const int off = r * 32 + ((qd ^ (r & 7)) << 2);  // floats, 128B-swizzled
-          float* hi = cb + opnd * 2 * BM * BK;
+          float* hi = cb + 2 * BM * BK;
           float* lo = hi + BM * BK;
           *(float4*)(hi + off) = h;
           *(float4*)(lo + off) = l;
         }
+        fence_before_sync();  // tcgen05.st (A) -> the MMA thread, via the mbarrier
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) {
@@ -448,14 +483,15 @@ static int get_enc32() {
 
 // Plain (non-swizzled) fp32 map over a column-major rows x cols matrix.
 static int make_map32(CUtensorMap* map, const float* p, long rows, long cols, long ld, uint32_t box0,
-                      uint32_t box1) {
+                      uint32_t box1, bool sw128 = false) {
   if ((ld & 3) || ((uintptr_t)p & 15)) return UTV_ERR_ALIGN;
   cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)cols};
   cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
   cuuint32_t box[2] = {box0, box1};
   cuuint32_t es[2] = {1, 1};
   CUresult r = g_enc32(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)p, dims, strides, box, es,
-                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       sw128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     fprintf(stderr, "libutvb200: fp32 tensor map failed (%d) rows=%ld cols=%ld ld=%ld\n", (int)r,
@@ -489,7 +525,7 @@ int sgemm_tf32x3(bool ta, bool tb, int M, int N, int K, float alpha, const float
   if (((uintptr_t)C & 3) || ldc < M) return UTV_ERR_ALIGN;
   CUtensorMap mA, mB;
   // A (op(A) is M x K): TA -> stored K x M (K contiguous); else M x K (M contiguous)
-  if (ta) UTV_CHECK(make_map32(&mA, A, K, M, lda, tf32::BK, tf32::BM));
+  if (ta) UTV_CHECK(make_map32(&mA, A, K, M, lda, tf32::BK, tf32::BM, true));  // rows read per lane
   else UTV_CHECK(make_map32(&mA, A, M, K, lda, tf32::BM, tf32::BK));
   // B (op(B) is K x N): !TB -> stored K x N (K contiguous); else N x K (N contiguous)
   if (!tb) UTV_CHECK(make_map32(&mB, B, K, N, ldb, tf32::BK, tf32::BN));
