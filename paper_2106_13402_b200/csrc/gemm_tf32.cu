@@ -37,7 +37,7 @@ namespace utv {
 
 namespace tf32 {
 constexpr int BM = 128, BN = 128, BK = 32;
-constexpr int RAW_STAGES = 2, CONV_STAGES = 2, ACC_STAGES = 2;
+constexpr int RAW_STAGES = 4, CONV_STAGES = 2, ACC_STAGES = 2;
 constexpr int THREADS = 896;                  // 28 warps
 constexpr int CONV_WARP0 = 4, NCONV = 8;      // converter warps 4..11
 constexpr int EPI_WARP0 = 12;                 // epilogue warps 12..27 (4 per TMEM lane quarter)
@@ -45,7 +45,7 @@ constexpr int EPI_COLS = 32;                  // accumulator columns per epilogu
 constexpr int CHUNK_KB = 16;                  // k-blocks (512 k) per TMEM accumulation chunk
 constexpr uint32_t TILE_BYTES = BM * BK * 4;  // 16 KB (A or B, raw or hi or lo)
 constexpr uint32_t RAW_BYTES = 2 * TILE_BYTES;
-constexpr uint32_t CONV_BYTES = 4 * TILE_BYTES;  // hiA loA hiB loB
+constexpr uint32_t CONV_BYTES = 2 * TILE_BYTES;  // hiB loB (A's hi/lo live in TMEM)
 constexpr size_t SMEM = (size_t)RAW_STAGES * RAW_BYTES + (size_t)CONV_STAGES * CONV_BYTES + 1024 + 512;
 constexpr uint32_t SUM_COL = ACC_STAGES * BN;   // running chunk sum (128 columns) after the buffers
 constexpr uint32_t A_COL = SUM_COL + BN;         // A operand hi|lo per conversion stage (2 x 64 columns)
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (lane == 0) {
           const uint32_t tmem_d = tmem_base + as * BN;
           const uint32_t base = smem_u32(conv + c * CONV_BYTES);
-          const uint32_t hiB = base + 2 * TILE_BYTES, loB = base + 3 * TILE_BYTES;
+          const uint32_t hiB = base, loB = base + TILE_BYTES;
           const uint32_t hiA = tmem_base + A_COL + c * 2 * BK, loA = hiA + BK;  // TMEM columns
 #pragma unroll
           for (int ks = 0; ks < BK / 8; ++ks) {
@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           h.z = rna_tf32(x.z); l.z = x.z - h.z;
           h.w = rna_tf32(x.w); l.w = x.w - h.w;
           const int off = r * 32 + ((qd ^ (r & 7)) << 2);  // floats, 128B-swizzled
-          float* hi = cb + 2 * BM * BK;
+          float* hi = cb;
           float* lo = hi + BM * BK;
           *(float4*)(hi + off) = h;
           *(float4*)(lo + off) = l;
