@@ -12,20 +12,28 @@
 //
 // Design (sm_100a, warp-specialised, persistent):
 //   warp 0      TMA producer: raw fp32 tiles A (128 x 32) and B (128 x 32)
-//               into a RAW_STAGES ring (mbarrier full/empty, expect_tx)
+//               into a RAW_STAGES ring (mbarrier full/empty, expect_tx);
+//               K-major A tiles arrive 128B-swizzled
 //   warp 1      TMEM allocator + MMA issuer (one elected lane):
 //               12 x tcgen05.mma.cta_group::1.kind::tf32 (M=128, N=128, K=8)
-//               per 32-deep k-block, tcgen05.commit -> mbarriers
-//   warps 4-11  converters: raw tile (K- or MN-major) -> hi / lo tiles in
-//               the canonical K-major 128B-swizzled UMMA layout (also turns
-//               MN-major operands K-major, so one descriptor form serves all
-//               four op combinations); fence.proxy.async before arrival
+//               per 32-deep k-block, A from TMEM, B from shared memory,
+//               tcgen05.commit -> mbarriers
+//   warps 4-11  converters: A rows -> hi / lo straight into TMEM
+//               (tcgen05.st, each warp in its lane quarter, 16 k columns);
+//               B (K- or MN-major) -> hi / lo tiles in the canonical K-major
+//               128B-swizzled UMMA layout in shared memory;
+//               tcgen05.fence + fence.proxy.async before arrival
 //   warps 12-27 epilogue: tcgen05.ld 32x32b from a double-buffered TMEM
 //               accumulator (2 x 128 columns).  The tensor-core FP32
 //               accumulator does not round to nearest, so K is split into
-//               512-deep chunks whose partial tiles are summed in registers
-//               (RN) — long-K products stay fp32-accurate; alpha/beta,
-//               coalesced stores; overlaps the next tile's MMAs.
+//               512-deep chunks folded with round-to-nearest adds into a
+//               running sum in TMEM — long-K products stay fp32-accurate;
+//               alpha/beta, coalesced stores; overlaps the next tile's MMAs.
+// TMEM (512 columns): [0, 256) accumulators, [256, 384) running sum,
+// [384, 512) A hi|lo for the two conversion stages.  Moving A's split out of
+// shared memory halved the converters' smem stores, which had saturated
+// the L1/smem pipe (l1tex 81% -> 57%).  16 converter warps (8 epilogue)
+// measured slower (C5 sampling GEMM 186 -> 173 TF/s useful).
 #include <cudaTypedefs.h>
 
 #include <mutex>
