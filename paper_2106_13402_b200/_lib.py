@@ -8,6 +8,7 @@ compute entry point raises ``RuntimeError``.
 from __future__ import annotations
 
 import ctypes
+import threading
 import os
 from dataclasses import dataclass
 
@@ -198,6 +199,27 @@ class DMat:
 # into the destination numpy array is several times faster and needs no
 # large page-locked allocation.
 _RING = None
+# The pinned staging rings are process-wide; the public API is re-entrant
+# (utvkit's functions are pure), so each ring is used under its own lock —
+# concurrent calls from several host threads serialise their staging.
+_RING_LOCK = threading.Lock()
+# One device pipeline at a time: the drivers share library-owned side
+# streams, events and tile-scheduler slots, so public calls made from
+# several host threads run one after another (re-entrant: rurv -> power_urv).
+_API_LOCK = threading.RLock()
+
+
+def serialized(fn):
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(*args, **kwargs):
+        with _API_LOCK:
+            return fn(*args, **kwargs)
+    return wrapper
+
+_H2D_LOCK = threading.Lock()
+_ASYNC_LOCK = threading.Lock()
 _RING_CHUNK = 64 << 20
 _POOL = None
 
@@ -254,6 +276,11 @@ def _h2d_bytes(src, dst, stream, nthr=8):
     an nthr-way host memcpy into a pinned ring buffer, then its DMA on
     `stream`, chunks pipelined so the memcpy of chunk i+1 overlaps the DMA
     of chunk i (a pageable copy_ runs at ~10 GB/s on the B200 hosts)."""
+    with _H2D_LOCK:
+        _h2d_bytes_locked(src, dst, stream, nthr)
+
+
+def _h2d_bytes_locked(src, dst, stream, nthr):
     global _H2D_RING
     import torch
     if _H2D_RING is None:
@@ -295,7 +322,8 @@ def d2h_numpy(m):
     out = np.empty((m.rows, m.cols), dtype=dt, order="F")
     dst = out.reshape(-1, order="F").view(np.uint8)
     src = m.t.view(-1)[m.off: m.off + m.rows * m.cols].view(torch.uint8)
-    _d2h_bytes(src, dst, torch.cuda.current_stream(), ring, pool)
+    with _RING_LOCK:
+        _d2h_bytes(src, dst, torch.cuda.current_stream(), ring, pool)
     return out
 
 
@@ -380,7 +408,8 @@ class AsyncD2H:
                         dst = host.reshape(-1, order="F")[c0 * m.rows: c1 * m.rows].view(np.uint8)
                         assert m.ld == m.rows and dst.nbytes == src.numel() and es == host.itemsize
                         self._wait_faults(host, c0 * m.rows * es, c1 * m.rows * es)
-                        _d2h_bytes(src, dst, self.stream, self.ring, self.pool)
+                        with _ASYNC_LOCK:
+                            _d2h_bytes(src, dst, self.stream, self.ring, self.pool)
             except BaseException as e:  # surfaced by finish()
                 self.err = e
 

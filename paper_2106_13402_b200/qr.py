@@ -9,6 +9,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from ._lib import serialized as _serialized
 from . import device as dv
 from ._lib import dfrom_numpy
 from .errors import DimensionError
@@ -37,6 +38,7 @@ class PivotedQr:
     perm: np.ndarray
 
 
+@_serialized
 def hqr_full(a):
     """Full unpivoted Householder QR (m >= n) -> (QFactor, R); qr.py:71-100."""
     a = check_matrix(a)
@@ -48,6 +50,7 @@ def hqr_full(a):
     return QFactor(Y=Y.to_numpy(), Twy=T.to_numpy(), m=m), d.to_numpy()
 
 
+@_serialized
 def apply_q(q, b, side="left", trans=False):
     """Q @ b, Q.T @ b (left) or b @ Q, b @ Q.T (right), three GEMMs; qr.py:103-121."""
     b = np.asarray(b, dtype=np.float64)
@@ -68,6 +71,7 @@ def apply_q(q, b, side="left", trans=False):
     return d.to_numpy()
 
 
+@_serialized
 def materialize_q(q, ncols=None):
     """Leading ncols columns of Q (all m by default); qr.py:124-131."""
     ncols = q.m if ncols is None else int(ncols)
@@ -76,6 +80,7 @@ def materialize_q(q, ncols=None):
     return dv.orgqr(dfrom_numpy(q.Y), dfrom_numpy(q.Twy), ncols).to_numpy()
 
 
+@_serialized
 def hqr_thin(a):
     """Thin QR: (Qhat m x n orthonormal, Rhat n x n); qr.py:134-138."""
     q, r = hqr_full(a)
@@ -83,6 +88,7 @@ def hqr_thin(a):
     return materialize_q(q, ncols=n), np.array(r[:n, :], copy=True)
 
 
+@_serialized
 def hqrcp(a):
     """Column-pivoted Householder QR (greedy largest-norm pivoting) — the
     paper's comparator, qr.py:152-204, as one persistent cooperative kernel

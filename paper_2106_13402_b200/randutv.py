@@ -15,6 +15,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from ._lib import serialized as _serialized
 from . import device as dv
 from ._lib import deye, dfrom_numpy
 from .errors import ConsistencyError, ConvergenceError, DimensionError
@@ -131,6 +132,7 @@ def randutv_basic_device32(t_dev, b, q, g_dev, record_trailing=False):
     return run, U, V
 
 
+@_serialized
 def randutv_basic(a, b, q, rng, record_trailing=False, *, dtype=np.float64):
     """Blocked randomized UTV without oversampling (randutv.py:228-235).
 
@@ -344,6 +346,7 @@ def _randutv_basic_pipelined(a, b, q, rng, record_trailing):
     return _finish_basic(a, b, q, run, t_dev, U, V, record_trailing, False, host=out, anorm=anorm)
 
 
+@_serialized
 def randutv_boosted(a, b, q, p, rng, record_trailing=False):
     """Algorithm 2: oversampling + sample recycling (randutv.py:238-247)."""
     if q < 1:
@@ -351,6 +354,7 @@ def randutv_boosted(a, b, q, p, rng, record_trailing=False):
     return _randutv_stepwise(a, b, q, p, rng, boosted=True, record_trailing=record_trailing)
 
 
+@_serialized
 def randutv_partial(a, b, q, p, rng, tol_fro=None, max_rank=None, record_trailing=False):
     """Boosted randUTV halted by error tolerance or column budget (randutv.py:250-264)."""
     if q < 1:

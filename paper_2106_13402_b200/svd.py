@@ -12,6 +12,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from ._lib import serialized as _serialized
 from . import device as dv
 from ._lib import dfrom_numpy
 from .errors import ConvergenceError
@@ -46,6 +47,7 @@ def _sign_fix(u, v):
             u[:, j] = -u[:, j]
 
 
+@_serialized
 def svd_dense(a, mode="full"):
     """Dense SVD with deterministic signs (svd.py:37-58)."""
     a = check_matrix(a)

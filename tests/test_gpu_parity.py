@@ -182,3 +182,34 @@ def test_randutv_boosted_partial_match_reference(golden, name):
     assert orc.orthogonality(f.V) < 1e-13 * a.shape[1]
     assert np.allclose(f.errors, g["errors"], rtol=1e-8, atol=1e-7 * np.linalg.norm(a))
     assert np.allclose(f.trailing_fro, g["trailing"], rtol=1e-9, atol=1e-12 * np.linalg.norm(a))
+
+
+def test_public_api_concurrent_threads_match_sequential():
+    """The reference API is pure and re-entrant: calls made from several host
+    threads at once (sharing the library's side streams and the pinned
+    staging rings) return exactly what the same calls return one by one."""
+    import threading
+
+    import paper_2106_13402_b200 as pk
+    rng = np.random.default_rng(77)
+    a1 = np.asfortranarray(rng.standard_normal((2048, 2048)) * np.exp(-np.arange(2048) / 300.0))
+    a2 = np.asfortranarray(rng.standard_normal((1100, 1100)))
+
+    def job_purv():
+        return pk.power_urv(a1, 1, pk.RngStream(5))
+
+    def job_rutv():
+        return pk.randutv_basic(a2, 128, 1, pk.RngStream(6))
+
+    seq = [job_purv(), job_rutv()]
+    out = [None, None]
+
+    def run(i, f):
+        out[i] = f()
+    ths = [threading.Thread(target=run, args=(0, job_purv)), threading.Thread(target=run, args=(1, job_rutv))]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert np.array_equal(out[0].R, seq[0].R) and np.array_equal(out[0].Vq.Y, seq[0].Vq.Y)
+    assert np.array_equal(out[1].T, seq[1].T) and np.array_equal(out[1].U, seq[1].U)
