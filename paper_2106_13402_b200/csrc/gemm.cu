@@ -28,6 +28,7 @@
 //    MxN tile count cannot fill 148 SMs.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include "common.cuh"
@@ -384,16 +385,35 @@ __global__ void __launch_bounds__(THREADS, 1)
 __global__ void splitk_reduce_kernel(const double* __restrict__ ws, int splits, int M, int N,
                                      double alpha, double beta, double* C, long ldc,
                                      int tri_ksplit) {
+  // 2-D walk (column n, row pair m, m+1): no 64-bit index division per
+  // element, 16-byte partial loads (the workspace has ld = M, M even here
+  // or the pair degrades to one row), all splits' loads in flight together.
   const size_t total = (size_t)M * N;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
-       i += (size_t)gridDim.x * blockDim.x) {
-    const int m = (int)(i % M), n = (int)(i / M);
-    const int z0 = tri_ksplit > 0 ? ((m / BM) * BM / BK * BK) / tri_ksplit : 0;
-    double s = 0.0;
-    for (int z = z0; z < splits; ++z) s += ws[(size_t)z * total + i];
-    double* c = C + m + (long)n * ldc;
-    const double v = alpha * s;
-    *c = (beta == 0.0) ? v : fma(beta, *c, v);
+  const int pairs = (M + 1) >> 1;
+  const bool vec = (M & 1) == 0;
+  for (int n = blockIdx.y; n < N; n += gridDim.y) {
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < pairs; p += gridDim.x * blockDim.x) {
+      const int m = 2 * p;
+      const int z0 = tri_ksplit > 0 ? ((m / BM) * BM / BK * BK) / tri_ksplit : 0;  // m, m+1: same tile
+      const size_t i = (size_t)n * M + m;
+      double s0 = 0.0, s1 = 0.0;
+      if (vec) {
+#pragma unroll 4
+        for (int z = z0; z < splits; ++z) {
+          const double2 w = __ldcs((const double2*)(ws + (size_t)z * total + i));
+          s0 += w.x;
+          s1 += w.y;
+        }
+      } else {
+        for (int z = z0; z < splits; ++z) {
+          s0 += __ldcs(ws + (size_t)z * total + i);
+          if (m + 1 < M) s1 += __ldcs(ws + (size_t)z * total + i + 1);
+        }
+      }
+      double* c = C + m + (long)n * ldc;
+      c[0] = (beta == 0.0) ? alpha * s0 : fma(beta, c[0], alpha * s0);
+      if (m + 1 < M) c[1] = (beta == 0.0) ? alpha * s1 : fma(beta, c[1], alpha * s1);
+    }
   }
 }
 
@@ -701,8 +721,10 @@ int dgemm_ex(bool ta, bool tb, int M, int N, int K, double alpha, const double* 
   if (use_ws) {
     const long total = (long)M * N;
     ProfScope ps(PROF_SPLITK, 0.0, 8.0 * (splits + (beta != 0.0 ? 2 : 1)) * total, st);
-    gemm::splitk_reduce_kernel<<<min(8 * num_sms(), ceil_div(total, 256)), 256, 0, st>>>(
-        ws, splits, M, N, alpha, beta, C, ldc, tri ? kper : 0);
+    const int gx = ceil_div(ceil_div(M, 2), 256);
+    const int gy = (int)std::min<long>(N, std::max<long>(1, 8L * num_sms() / gx));
+    gemm::splitk_reduce_kernel<<<dim3(gx, gy), 256, 0, st>>>(ws, splits, M, N, alpha, beta, C, ldc,
+                                                            tri ? kper : 0);
     UTV_CUDA(cudaGetLastError());
   }
   if (ctmp) UTV_CUDA(cudaFreeAsync(ctmp, st));
