@@ -42,6 +42,15 @@ def test_argument_validation_without_device():
     assert lib.utv_dgeqrf(3, 4, 0, 4, 0, 4, 0, 4, 0, 0, 0) == -2          # n > m
     assert lib.utv_randutv_basic_f64(4, 4, 0, 1, 0, 4, 0, 4, 0, 4, 0, 4, 0, 0, 0, 0, 0, 0) == -3
     assert lib.utv_powerurv_f64(4, 4, -1, 0, 4, 0, 4, 0, 4, 0, 4, 0, 4, 0, 4, 0, 4, 0, 0, 0) == -3
+    # the Yhat-seeded entry: q >= 1, Yhat required, LAPACK-style indices
+    yh = [4, 4, 1, 0, 4, 8, 4, 0, 4, 0, 4, 0, 4, 0, 4, 0, 4, 0, 0, 0, None, None]
+    assert lib.utv_powerurv_f64_yhat(*(yh[:2] + [0] + yh[3:])) == -3       # q = 0
+    assert lib.utv_powerurv_f64_yhat(*(yh[:5] + [0] + yh[6:])) == -6       # Yhat null
+    assert lib.utv_powerurv_f64_yhat(*(yh[:6] + [3] + yh[7:])) == -7       # ldy0 < m
+    assert lib.utv_powerurv_f64_yhat(5, 6, *yh[2:]) == -2                  # n > m
+    # both event arguments of the _ev entry are optional
+    assert lib.utv_powerurv_f64_ev(4, 4, -1, 0, 4, 0, 4, 0, 4, 0, 4, 0, 4, 0, 4, 0, 4, 0, 0, 0,
+                                   None, None) == -3
 
 
 def test_flop_model_matches_survey():
