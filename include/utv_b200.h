@@ -205,8 +205,9 @@ int utv_powerurv_f64_ev(int m, int n, int q, const double* A, long lda, const do
                         double* Uy, long lduy, double* Ut, long ldut, double* R, long ldr,
                         double* Vy, long ldvy, double* Vt, long ldvt, void* work, size_t lwork,
                         void* stream, void* vq_ready, void* r_ready);
-/* Same with q >= 1 and the first power-round product Yhat = A G supplied by
- * the caller (m x n, device, read only) instead of G: the public power_urv
+/* power_urv (powerurv.py:75-79 -> power_urv_from_sample :41-72, its first
+ * product :64 supplied): q >= 1 and Yhat = A G given by the caller
+ * (m x n, device, read only) instead of G: the public power_urv
  * forms it as K-chunked products while G is still being drawn on the host
  * (row block by row block of the reference's C-order draw), so the host
  * RNG overlaps the device. */
