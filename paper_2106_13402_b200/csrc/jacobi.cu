@@ -184,7 +184,8 @@ __global__ void __launch_bounds__(1024) jacobi_finish_kernel(const double* __res
                                                             const double* __restrict__ V,
                                                             long ld, int n, double* sigma,
                                                             double* U, long ldu, double* Vo,
-                                                            long ldv, double* scratch) {
+                                                            long ldv, double* scratch,
+                                                            int sign_on_u) {
   extern __shared__ double sm[];
   double* sig = sm;            // n
   int* perm = (int*)(sig + n);  // n
@@ -265,12 +266,15 @@ __global__ void __launch_bounds__(1024) jacobi_finish_kernel(const double* __res
     }
   }
   __syncthreads();
-  // sign rule: first argmax |V[:, k]| must be positive
+  // sign rule: first argmax |V[:, k]| must be positive (V of the caller's
+  // matrix: the U output here when the rounds ran on its transpose)
+  const double* Sg = sign_on_u ? U : Vo;
+  const long lds = sign_on_u ? ldu : ldv;
   for (int k = warp; k < n; k += nw) {
     double best = -1.0;
     int bi = n;
     for (int i = lane; i < n; i += 32) {
-      const double v = fabs(Vo[i + (long)k * ldv]);
+      const double v = fabs(Sg[i + (long)k * lds]);
       if (v > best) { best = v; bi = i; }
     }
 #pragma unroll
@@ -279,7 +283,7 @@ __global__ void __launch_bounds__(1024) jacobi_finish_kernel(const double* __res
       const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
       if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
     }
-    const bool flip = Vo[bi + (long)k * ldv] < 0.0;
+    const bool flip = Sg[bi + (long)k * lds] < 0.0;
     __syncwarp();
     if (flip)
       for (int i = lane; i < n; i += 32) {
@@ -332,8 +336,19 @@ int gesvj(Mat A, double* sigma, Mat U, Mat V, double* ws, size_t ws_doubles, int
   if (!scratch) return UTV_ERR_WORKSPACE;
   // rows are padded to an even count (16-byte vector moves); padding is zero
   const int ne = n + (n & 1);
+  // The rounds run on A^T (UTV_JAC_TRANSPOSE, default on): for the graded
+  // upper-triangular blocks randUTV hands in, the columns of R^T start much
+  // closer to orthogonal, so far fewer rotations fire (256^2 Gaussian-decay
+  // block 6.2 -> 2.8 ms, tools/jacobi_transpose_probe.py).  A^T = W S X^T
+  // gives A = X S W^T: the outputs swap (U <- normalised columns, with the
+  // null-column completion, goes to V; W goes to U) and the sign rule reads V.
+  static const bool tr = [] {
+    const char* e = getenv("UTV_JAC_TRANSPOSE");
+    return e ? atoi(e) != 0 : true;
+  }();
   UTV_CHECK(set_zero(Aw, ld, (int)ld, (int)npad, st));
-  UTV_CHECK(copy_mat(A.p, A.ld, Aw, ld, n, n, st));
+  if (tr) UTV_CHECK(transpose(A.p, A.ld, Aw, ld, n, n, st));
+  else UTV_CHECK(copy_mat(A.p, A.ld, Aw, ld, n, n, st));
   UTV_CHECK(set_zero(Vw, ld, (int)ld, (int)npad, st));
   UTV_CHECK(set_identity(Vw, ld, n, n, st));
   UTV_CUDA(cudaMemsetAsync(ctl, 0, (jac::MAX_SWEEPS + 64) * sizeof(double), st));
@@ -367,8 +382,12 @@ int gesvj(Mat A, double* sigma, Mat U, Mat V, double* ws, size_t ws_doubles, int
   }
   const size_t smem2 = (size_t)4 * (n + 2) * sizeof(double);
   ProfScope ps2(PROF_JFINISH, 0.0, 0.0, st);
-  jac::jacobi_finish_kernel<<<1, 1024, smem2, st>>>(Aw, Vw, ld, n, sigma, U.p, U.ld, V.p, V.ld,
-                                                    scratch);
+  if (tr)
+    jac::jacobi_finish_kernel<<<1, 1024, smem2, st>>>(Aw, Vw, ld, n, sigma, V.p, V.ld, U.p, U.ld,
+                                                      scratch, 1);
+  else
+    jac::jacobi_finish_kernel<<<1, 1024, smem2, st>>>(Aw, Vw, ld, n, sigma, U.p, U.ld, V.p, V.ld,
+                                                      scratch, 0);
   UTV_CUDA(cudaGetLastError());
   return UTV_OK;
 }
