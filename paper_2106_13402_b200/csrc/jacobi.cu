@@ -298,6 +298,12 @@ __global__ void __launch_bounds__(1024) jacobi_finish_kernel(const double* __res
 // fit the 200 KB smem budget: 4 W n 8 bytes.
 static inline int jac_width(int n) {
   const int ne = n + (n & 1);
+  static const int forced = [] {  // tuning knob: UTV_JAC_W = 4 / 8 / 16
+    const char* e = getenv("UTV_JAC_W");
+    return e ? atoi(e) : 0;
+  }();
+  if ((forced == 4 || forced == 8 || forced == 16) && (size_t)4 * forced * ne * 8 <= 200 * 1024)
+    return forced;
   if ((size_t)4 * 16 * ne * 8 <= 200 * 1024) return 16;
   if ((size_t)4 * 8 * ne * 8 <= 200 * 1024) return 8;
   return 4;
