@@ -334,7 +334,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     // over the prefetched C tile in smem and leaves by one TMA store, so the
     // warps start the next tile without draining 128 KB of stores first.
     // (tile origins at a -1 row/column shift keep the direct stores)
-    const bool tstore = HASC && p.c_sh == 0 && !w && m0 >= 0 && n0 >= 0;
+    // A TMA store writes whole 16-byte granules: with an odd row count the
+    // granule holding row M-1 also covers row M, outside the matrix, so the
+    // tile containing the last row of an odd-M matrix keeps the direct stores.
+    const bool tstore = HASC && p.c_sh == 0 && !w && m0 >= 0 && n0 >= 0 &&
+                        ((p.M & 1) == 0 || m0 + BM <= p.M);
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
       const int ml = frag_row<TA>(wm, t, fr);

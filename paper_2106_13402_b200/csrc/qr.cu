@@ -30,8 +30,10 @@ constexpr int PANEL = QR_PANEL;  // outer panel width
 // K2: B <- Q^(T) B (side L) or B Q^(T) (side R), Q = I - Y T Y^T.
 // ---------------------------------------------------------------------------
 size_t larfb_ws_doubles(int brows, int bcols, int w) {
+  // two W buffers of round_up(w, 4) x other (side L) or round_up(rows, 4) x w
+  // (side R) doubles: both leading dimensions are padded to 4
   const long other = brows > bcols ? brows : bcols;
-  return 2 * (size_t)w * other + 512 + SPLITK_WS;
+  return 2 * (size_t)round_up(w, 4) * round_up(other, 4) + 512 + SPLITK_WS;
 }
 
 int larfb(char side, bool trans, Mat Y, Mat T, Mat B, double* ws, size_t ws_doubles,

@@ -195,3 +195,31 @@ def test_dgemm_parity_offsets_all_ops(dv, ta, tb, ra, rb):
                         dB.at(rb, 5), dB.ld, 0.0, C.ptr, C.ld, ws.data_ptr(), lw, stream_ptr()), "dgemm")
     ref = (A.T if ta else A) @ (B.T if tb else B)
     assert np.abs(C.to_numpy() - ref).max() < 1e-12 * k
+
+
+@pytest.mark.parametrize("M,N,K,ta,tb,beta", [(20001, 300, 256, "N", "N", 1.0), (20001, 44, 256, "N", "T", 1.0),
+                                               (20003, 200, 512, "N", "N", 1.0), (3001, 300, 64, "T", "N", 1.0),
+                                               (20001, 44, 256, "N", "N", 0.0)])
+def test_gemm_writes_stay_inside_the_view(M, N, K, ta, tb, beta):
+    """C is a view on the top rows of a taller buffer (a TSQR row chunk): no
+    kernel may write below it — a TMA store of an odd-M tile once did (its
+    16-byte granule covered row M)."""
+    import torch
+    import paper_2106_13402_b200.device as dv
+    from paper_2106_13402_b200._lib import dempty
+    big = dempty(M + 64, N)
+    big.t.normal_()
+    C = big.sub(0, 0, M, N)
+    A = dempty(K if ta == "T" else M, M if ta == "T" else K)
+    A.t.normal_()
+    B = dempty(N if tb == "T" else K, K if tb == "T" else N)
+    B.t.normal_()
+    view = lambda d: d.tensor().T
+    below = view(big)[M:M + 64, :N].clone()
+    c0 = view(C)[:M, :N].clone()
+    a, b = view(A)[:A.rows, :A.cols], view(B)[:B.rows, :B.cols]
+    ref = -((a.T if ta == "T" else a) @ (b.T if tb == "T" else b)) + beta * c0
+    dv.gemm(ta, tb, -1.0, A, B, beta, C)
+    torch.cuda.synchronize()
+    assert torch.equal(view(big)[M:M + 64, :N], below)
+    assert ((view(C)[:M, :N] - ref).abs().max() / ref.abs().max()).item() < 1e-13

@@ -134,6 +134,42 @@ def test_power_urv_streamed_draw_matches_from_sample(m, n, q):
     assert np.abs(f.Vq.Twy - ref.Vq.Twy).max() < 1e-8
 
 
+@pytest.mark.parametrize("m,n,q", [(1001, 300, 1), (1002, 301, 2), (1003, 257, 1), (1005, 1005, 1),
+                                   (1006, 700, 0)])
+def test_power_urv_ragged_rows_against_oracle(m, n, q):
+    """Row counts that are not a multiple of 4 (the device buffers pad their
+    leading dimensions; the compact-WY workspaces must account for that)."""
+    import paper_2106_13402_b200 as pk
+    a, d = orc.decay_matrix(n, 1e-5, seed=m + q, m=m)
+    g = orc.draw_gaussian(orc.gaussian_stream(m), n, n)
+    ref = orc.power_urv(a, q, g)
+    f = pk.power_urv_from_sample(a, q, g)
+    assert _mixed_ok(np.diag(f.R), np.diag(ref["R"]), d[0])
+    assert np.abs(f.Vq.Y - ref["Vy"]).max() < 1e-8
+    assert np.abs(f.Uq.Y - ref["Uy"]).max() < 1e-8
+
+
+@pytest.mark.parametrize("m,n,b", [(1002, 999, 128), (1001, 1001, 96), (1003, 513, 256)])
+def test_randutv_ragged_against_oracle(m, n, b):
+    import paper_2106_13402_b200 as pk
+    a, d = orc.decay_matrix(n, 1e-5, seed=m + b, m=m)
+    blocks = orc.randutv_sample_blocks(orc.gaussian_stream(b), m, n, b)
+    ref = orc.randutv_basic(a, b, 1, blocks)
+    f = pk.randutv_basic(a, b, 1, pk.RngStream(b))
+    # mid-block diag(T) entries of these shapes move by ~1e-9 relative when A
+    # is perturbed by one ulp (the oracle against itself), so the gate adds
+    # 8x that measured spread to the 1e-10 mixed tolerance (SURVEY §8c)
+    a2 = a * (1.0 + orc.EPS * np.random.default_rng(m).standard_normal(a.shape))
+    spread = np.abs(np.diag(orc.randutv_basic(a2, b, 1, blocks)["T"]) - np.diag(ref["T"]))
+    tol = 1e-10 * np.abs(np.diag(ref["T"])) + 16 * orc.EPS * d[0] + 8 * spread
+    assert np.all(np.abs(np.diag(f.T) - np.diag(ref["T"])) <= tol)
+    # tall input: U[:, n:] is a non-unique orthonormal completion (as with LAPACK)
+    assert np.abs(f.U[:, :n] - ref["U"][:, :n]).max() < 1e-8
+    assert np.abs(f.V - ref["V"]).max() < 1e-8
+    assert orc.reconstruction(a, f.U, f.T, f.V) < 1e-13
+    assert orc.orthogonality(f.U) < 1e-13 * m
+
+
 def test_api_errors_match_reference():
     import paper_2106_13402_b200 as pk
     with pytest.raises(pk.DimensionError):
