@@ -95,3 +95,25 @@ def test_sharded_thread_ranks_device(world, chunk):
         for k in ("Ut", "R", "Vy", "Vt"):
             assert np.array_equal(results[r][k], results[0][k])
     _check(out, orc.power_urv(a, q, g), a)
+
+
+def test_tsqr_odd_row_chunks_match_device_driver():
+    """Row chunks of odd height at odd offsets inside one buffer (the C4 P=1
+    leaves: 524288 rows -> 74899/74898-row chunks): every chunk's QR must leave
+    its neighbours untouched, so the chunked path gives the device driver's R."""
+    import torch
+    import paper_2106_13402_b200 as pk
+    import paper_2106_13402_b200.device as dv
+    from paper_2106_13402_b200 import _lib
+    from paper_2106_13402_b200._lib import dempty
+    from paper_2106_13402_b200.sharded import Comm, power_urv_sharded
+    m, n = 74898, 512
+    a = dempty(m, n)
+    a.t.normal_(generator=torch.Generator(device="cuda").manual_seed(40))
+    g = _lib.dfrom_numpy(pk.gaussian(n, n, pk.RngStream(4)))
+    run = dv.PowerUrvRun(m, n, 1)
+    run.run(a, g)
+    d_dev = torch.diagonal(run.R.tensor()[:n, :n]).abs()
+    res = power_urv_sharded(a, g, 1, Comm(), chunk_rows=37449)
+    d_sh = torch.diagonal(res["R"].tensor()).abs()
+    assert ((d_sh - d_dev).abs().max() / d_dev.max()).item() < 1e-13
