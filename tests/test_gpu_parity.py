@@ -149,7 +149,8 @@ def test_power_urv_ragged_rows_against_oracle(m, n, q):
     assert np.abs(f.Uq.Y - ref["Uy"]).max() < 1e-8
 
 
-@pytest.mark.parametrize("m,n,b", [(1002, 999, 128), (1001, 1001, 96), (1003, 513, 256)])
+@pytest.mark.parametrize("m,n,b", [(1002, 999, 128), (1001, 1001, 96), (1003, 513, 256), (700, 650, 33),
+                                   (515, 515, 61), (2000, 1500, 255)])
 def test_randutv_ragged_against_oracle(m, n, b):
     import paper_2106_13402_b200 as pk
     a, d = orc.decay_matrix(n, 1e-5, seed=m + b, m=m)
