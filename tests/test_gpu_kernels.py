@@ -223,3 +223,26 @@ def test_gemm_writes_stay_inside_the_view(M, N, K, ta, tb, beta):
     torch.cuda.synchronize()
     assert torch.equal(view(big)[M:M + 64, :N], below)
     assert ((view(C)[:M, :N] - ref).abs().max() / ref.abs().max()).item() < 1e-13
+
+
+@pytest.mark.parametrize("rows,cols", [(20001, 300), (37449, 300), (20001, 257), (9001, 600), (513, 512)])
+def test_geqrf_writes_stay_inside_the_view(rows, cols):
+    """geqrf on the top rows of a taller buffer (a TSQR chunk) leaves the rows
+    below untouched and still factors its view exactly (thin Q R = A)."""
+    import torch
+    import paper_2106_13402_b200.device as dv
+    from paper_2106_13402_b200._lib import dempty
+    view = lambda d: d.tensor().T
+    big = dempty(2 * rows + 1, cols)
+    big.t.normal_()
+    sub = big.sub(0, 0, rows, cols)
+    A = view(sub)[:rows, :cols].clone()
+    below = view(big)[rows:2 * rows + 1, :cols].clone()
+    Y, T = dv.geqrf(sub)
+    torch.cuda.synchronize()
+    assert torch.equal(view(big)[rows:2 * rows + 1, :cols], below)
+    Yd, Td, Rd = view(Y)[:rows, :cols], view(T)[:cols, :cols], torch.triu(view(sub)[:cols, :cols])
+    E = torch.zeros(rows, cols, device="cuda", dtype=torch.float64)
+    E[:cols] = torch.eye(cols, device="cuda", dtype=torch.float64)
+    Q = E - Yd @ (Td @ Yd[:cols].T)
+    assert ((Q @ Rd - A).abs().max() / A.abs().max()).item() < 1e-13
