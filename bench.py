@@ -7,11 +7,19 @@ factorisation of the same synthetic matrix, inputs resident in HBM.
 value = algorithmic FP64 FLOPs of both (SURVEY.md §8d model) / seconds.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload auto|headline|c2|c4|c5]
 
-N > 1 (torchrun): randUTV does not shard -> every rank runs an
-independent replica ("replicas only"; scaling "weak"), timed max over ranks.
---impl reference times the reference algorithm on the host cores (the CPU
-oracle port, oracle/utv_oracle.py) on a bounded sample of the workload.
+--gpus N > 1 without WORLD_SIZE in the environment re-launches this script
+under torchrun (N ranks, 127.0.0.1 rendezvous, NCCL_DEBUG=INFO unless set).
+With N > 1 ranks the primary line is the ROW-SHARDED C4 powerURV
+(524288 x 4096, q=1, strong scaling: the rows are split over the ranks,
+collectives inside libutvb200 over NCCL); the headline runs as independent
+replicas in a nested secondary object (randUTV does not shard).
+At N = 1 the headline is the primary line and a 1-GPU C4 run is nested as
+the scaling base.
+--impl reference times the GENUINE reference package (oracle/_ref, an
+unmodified copy of utvkit made by oracle/build_ref.py; the numpy port
+oracle/utv_oracle.py if the copy is absent) on the host cores.
 """
 
 from __future__ import annotations
@@ -139,76 +147,194 @@ def cpu_threads():
     return os.cpu_count() or 1
 
 
-def cpu_sample_run(rutv_n=1536, purv_n=512, b=256, q=2, seed=0):
-    """Reference algorithm (CPU oracle port) on a bounded sample; returns dict."""
-    from oracle import utv_oracle as orc
-    rng = np.random.default_rng(seed)
-    a = rng.standard_normal((rutv_n, rutv_n))
-    blocks = orc.randutv_sample_blocks(orc.gaussian_stream(3), rutv_n, rutv_n, b)
+def _reference_impl():
+    """(module, kind): the genuine reference copy (oracle/_ref) or the port."""
+    from oracle import build_ref
+    if build_ref.available():
+        return build_ref.load(), "reference"
+    from oracle import utv_oracle
+    return None, "port"
+
+
+def _ref_time_purv(uk, n, q=2, seed=0):
+    a = np.random.default_rng(seed).standard_normal((n, n))
+    if uk is None:
+        from oracle import utv_oracle as orc
+        g = orc.draw_gaussian(orc.gaussian_stream(2), n, n)
+        t0 = time.perf_counter()
+        orc.power_urv(a, q, g)
+        return time.perf_counter() - t0
     t0 = time.perf_counter()
-    orc.randutv_basic(a, b, q, blocks)
-    t1 = time.perf_counter()
-    ap = rng.standard_normal((purv_n, purv_n))
-    g = orc.draw_gaussian(orc.gaussian_stream(2), purv_n, purv_n)
-    t2 = time.perf_counter()
-    orc.power_urv(ap, q, g)
-    t3 = time.perf_counter()
+    uk.power_urv(a, q, uk.RngStream(2))                  # reference powerurv.py:75-79
+    return time.perf_counter() - t0
+
+
+def _ref_time_rutv(uk, n, b=256, q=2, seed=0):
+    a = np.random.default_rng(seed).standard_normal((n, n))
+    if uk is None:
+        from oracle import utv_oracle as orc
+        blocks = orc.randutv_sample_blocks(orc.gaussian_stream(3), n, n, b)
+        t0 = time.perf_counter()
+        orc.randutv_basic(a, b, q, blocks)
+        return time.perf_counter() - t0
+    t0 = time.perf_counter()
+    uk.randutv_basic(a, b, q, uk.RngStream(3))           # reference randutv.py:228-235
+    return time.perf_counter() - t0
+
+
+#: bounded sample of the headline workload timed on the host cores
+REF_RUTV_N, REF_PURV_N = 1536, 512
+
+
+def cpu_sample_run(uk=None, kind=None, rutv_n=REF_RUTV_N, purv_n=REF_PURV_N, b=256, q=2):
+    """One sample step of the reference on the host: randUTV(rutv_n) + powerURV(purv_n)."""
+    if kind is None:
+        uk, kind = _reference_impl()
+    tr = _ref_time_rutv(uk, rutv_n, b, q)
+    tp = _ref_time_purv(uk, purv_n, q)
     fl = randutv_flops(rutv_n, rutv_n, b, q) + powerurv_flops(purv_n, purv_n, q)
-    return dict(seconds=(t1 - t0) + (t3 - t2), flops=fl, rutv_s=t1 - t0, purv_s=t3 - t2,
-                sample=f"randUTV b={b} q={q} n={rutv_n} + powerURV q={q} n={purv_n}, "
-                       f"oracle/utv_oracle.py (numpy {np.__version__}, OpenBLAS threads)")
+    src = ("oracle/_ref/utvkit (unmodified reference copy)" if kind == "reference"
+           else "oracle/utv_oracle.py (numpy port)")
+    return dict(seconds=tr + tp, flops=fl, rutv_s=tr, purv_s=tp, kind=kind,
+                sample=f"randUTV b={b} q={q} n={rutv_n} + powerURV q={q} n={purv_n} on i.i.d. "
+                       f"N(0,1) input (runtime is data-independent, PAPER.md:843); {src}, "
+                       f"numpy {np.__version__}, OpenBLAS on all host threads")
 
 
-# ---------------------------------------------------------------------------
-# reference arm
-# ---------------------------------------------------------------------------
+def _fit_power_law(ns, ts):
+    """t = c n^alpha by least squares in log-log space."""
+    x, y = np.log(np.asarray(ns, float)), np.log(np.asarray(ts, float))
+    alpha, logc = np.polyfit(x, y, 1)
+    return float(np.exp(logc)), float(alpha)
 
-def run_reference(args):
-    ws, rank, _ = dist_env()
-    if ws > 1:
-        import torch.distributed as dist
-        dist.init_process_group("gloo")
-        if rank != 0:
-            dist.barrier()
-            dist.destroy_process_group()
-            return
-    for _ in range(args.warmup):
-        cpu_sample_run()
-    tot_s, tot_f = 0.0, 0.0
-    sample = None
-    for _ in range(args.steps):
-        r = cpu_sample_run()
-        tot_s += r["seconds"]
-        tot_f += r["flops"]
-        sample = r["sample"]
-    val = tot_f / tot_s / 1e12
+
+def _ref_time_tall(uk, n, aspect=128, q=1, seed=0):
+    """Reference power_urv_from_sample (powerurv.py:41-72) on a tall m = aspect*n matrix."""
+    m = aspect * n
+    a = np.random.default_rng(seed).standard_normal((m, n))
+    if uk is None:
+        from oracle import utv_oracle as orc
+        g = orc.draw_gaussian(orc.gaussian_stream(4), n, n)
+        t0 = time.perf_counter()
+        orc.power_urv(a, q, g)
+        return time.perf_counter() - t0
+    g = np.asfortranarray(uk.RngStream(4).standard_normal(n, n))
+    t0 = time.perf_counter()
+    uk.power_urv_from_sample(a, q, g)
+    return time.perf_counter() - t0
+
+
+def _ladder_line(args, kind, metric, config, full_flops, sample_flops, timed, ladder_fits, extra):
+    """Reference-arm JSON line: value = full-size FLOPs / extrapolated seconds."""
+    t_full = sum(c * x ** al for (c, al, x) in ladder_fits)
+    val = full_flops / t_full / 1e12
+    tot = sum(timed)
+    sample_val = sample_flops * len(timed) / tot / 1e12
     line = {
-        "impl": "reference", "metric": METRIC, "value": val, "unit": "TFLOP/s",
+        "impl": "reference", "metric": metric, "value": val, "unit": "TFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_dict(args),
-        "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cpu_threads(), "kind": "port",
-                         "sample": sample},
+        "ms_per_step": 1e3 * tot / len(timed), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
+        "value_kind": "extrapolated to the full config from a measured ladder (t = c n^alpha fit "
+                      "per algorithm, see 'ladder'); full-size CPU runs take hours to days",
+        "sample_value": sample_val, "extrapolated_seconds": t_full,
+        "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cpu_threads(), "kind": kind,
+                         "sample_value": sample_val},
         "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    line.update(extra)
+    return line
+
+
+def run_reference(args, wl="headline"):
+    ws, rank, _ = dist_env()
+    if ws > 1 and rank != 0:
+        return                                   # rank 0 alone runs the CPU arm
+    uk, kind = _reference_impl()
+    src = ("oracle/_ref/utvkit (unmodified reference copy)" if kind == "reference"
+           else "oracle/utv_oracle.py (numpy port)")
+    if wl == "c5":
+        print(json.dumps({"impl": "reference", "unavailable": "the reference is fp64-only "
+                          "(check_matrix casts to float64, matrix.py:42): no fp32 CPU path"}), flush=True)
+        return
+    if wl == "c4":
+        m, n = args.c4_rows, args.c4_cols
+        for _ in range(args.warmup):
+            _ref_time_tall(uk, 64)
+        timed = [_ref_time_tall(uk, 128) for _ in range(args.steps)]
+        lad = {128: float(np.median(timed)), 192: _ref_time_tall(uk, 192), 256: _ref_time_tall(uk, 256)}
+        c, al = _fit_power_law(list(lad), list(lad.values()))
+        line = _ladder_line(
+            args, kind, C4_METRIC,
+            {"workload": f"C4 powerURV q=1 on {m}x{n} fp64 (reference: one process, host cores)"},
+            powerurv_flops(m, n, 1), powerurv_flops(128 * 128, 128, 1), timed, [(c, al, n)],
+            {"ladder": {"tall m=128n, q=1, n -> s": {k: round(v, 3) for k, v in lad.items()},
+                        "fit": f"t = {c:.3g} n^{al:.2f}"},
+             "sample": f"power_urv_from_sample q=1 on 16384x128 i.i.d. N(0,1); {src}"})
+        print(json.dumps(line), flush=True)
+        return
+    if wl == "c2":
+        n, q = 8192, 2
+        for _ in range(args.warmup):
+            _ref_time_purv(uk, 256, q)
+        timed = [_ref_time_purv(uk, 384, q) for _ in range(args.steps)]
+        lad = {256: _ref_time_purv(uk, 256, q), 384: float(np.median(timed)), 512: _ref_time_purv(uk, 512, q)}
+        c, al = _fit_power_law(list(lad), list(lad.values()))
+        line = _ladder_line(
+            args, kind, C2_METRIC, {"workload": f"C2 powerURV q={q} on {n}x{n} fp64"},
+            powerurv_flops(n, n, q), powerurv_flops(384, 384, q), timed, [(c, al, n)],
+            {"ladder": {"powerURV q=2, n -> s": {k: round(v, 3) for k, v in lad.items()},
+                        "fit": f"t = {c:.3g} n^{al:.2f}"},
+             "sample": f"power_urv q=2 on 384x384 i.i.d. N(0,1); {src}"})
+        print(json.dumps(line), flush=True)
+        return
+    n, b, q = args.n, args.b, args.q
+    for _ in range(args.warmup):
+        cpu_sample_run(uk, kind, rutv_n=768, purv_n=256, b=b, q=q)
+    timed, tr, tp = [], [], []
+    sample = None
+    for _ in range(args.steps):
+        r = cpu_sample_run(uk, kind, b=b, q=q)
+        timed.append(r["seconds"])
+        tr.append(r["rutv_s"])
+        tp.append(r["purv_s"])
+        sample = r["sample"]
+    # ladder (SURVEY §8d): two more sizes per algorithm, fitted t = c n^alpha,
+    # extrapolated to the headline n (labelled as such; the full-size CPU runs
+    # take ~35 min (randUTV) and days (powerURV) on these hosts)
+    lad_r = {1024: _ref_time_rutv(uk, 1024, b, q), REF_RUTV_N: float(np.median(tr)),
+             2048: _ref_time_rutv(uk, 2048, b, q)}
+    lad_p = {384: _ref_time_purv(uk, 384, q), REF_PURV_N: float(np.median(tp)),
+             768: _ref_time_purv(uk, 768, q)}
+    cr, ar = _fit_power_law(list(lad_r), list(lad_r.values()))
+    cp, apw = _fit_power_law(list(lad_p), list(lad_p.values()))
+    c1 = _ref_time_rutv(uk, 2000, 128, 1)       # C1 (BASELINE configs[0]) timed directly
+    line = _ladder_line(
+        args, kind, METRIC, config_dict(args, 1),
+        randutv_flops(n, n, b, q) + powerurv_flops(n, n, q),
+        randutv_flops(REF_RUTV_N, REF_RUTV_N, b, q) + powerurv_flops(REF_PURV_N, REF_PURV_N, q),
+        timed, [(cr, ar, n), (cp, apw, n)],
+        {"ladder": {"randUTV b=256 q=2, n -> s": {k: round(v, 3) for k, v in lad_r.items()},
+                    "randUTV fit": f"t = {cr:.3g} n^{ar:.2f} -> {cr * n ** ar:.0f} s at n={n}",
+                    "powerURV q=2, n -> s": {k: round(v, 3) for k, v in lad_p.items()},
+                    "powerURV fit": f"t = {cp:.3g} n^{apw:.2f} -> {cp * n ** apw:.0f} s at n={n}"},
+         "sample": sample,
+         "c1_seconds": c1,
+         "c1": "randUTV b=128 q=1 on 2000x2000 (BASELINE configs[0]), measured directly"})
     print(json.dumps(line), flush=True)
-    if ws > 1:
-        import torch.distributed as dist
-        dist.barrier()
-        dist.destroy_process_group()
 
 
 METRIC = "powerURV(q=2)+randUTV(b=256,q=2) fp64 n=16384: FP64 TFLOP/s (algorithmic, SURVEY §8d)"
 
 
-def config_dict(args):
+def config_dict(args, ws=None):
+    ws = args.gpus if ws is None else ws
     return {"workload": f"powerURV q={args.q} + randUTV basic b={args.b} q={args.q} on "
                         f"{args.n}x{args.n} fp64 (BASELINE configs C3 + powerURV n=16384 target)",
             "n": args.n, "b": args.b, "q": args.q,
             "matrix": "A = Q1 diag(d) Q2^T, d_i = max(exp(-((i-1)/(n/4))^2), 1e-5) (Gaussian decay)",
             "l2_policy": "inputs (2 GiB/matrix) larger than the 126 MB L2; no explicit flush",
-            "parallelism": f"replicas x{args.gpus}" if args.gpus > 1 else "1 GPU"}
+            "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"}
 
 
 # ---------------------------------------------------------------------------
@@ -236,19 +362,82 @@ def make_decay_matrix(n, seed):
     return a
 
 
-def run_ours(args):
+def _init_dist(ws, local):
     import torch
-    ws, rank, local = dist_env()
     if ws > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if not dist.is_initialized():
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+
+def _sync_all(ws):
+    import torch
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+
+def _max_over_ranks(ws, x):
+    if ws == 1:
+        return x
+    import torch
+    tt = torch.tensor([x], device="cuda", dtype=torch.float64)
+    torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+    return float(tt.item())
+
+
+def _lib_copy(src, dst):
+    from paper_2106_13402_b200 import _lib
+    _lib.check(_lib.load().utv_dlacpy(src.rows, src.cols, src.ptr, src.ld, dst.ptr, dst.ld,
+                                      _lib.stream_ptr()), "utv_dlacpy")
+
+
+def _lib_eye(m):
+    from paper_2106_13402_b200 import _lib
+    _lib.check(_lib.load().utv_dlaset(b"A", m.rows, m.cols, 0.0, 1.0, m.ptr, m.ld,
+                                      _lib.stream_ptr()), "utv_dlaset")
+
+
+def _panel_columns(n, b, q):
+    """Householder columns factored by the panel kernel per headline step:
+    randUTV 2 b-wide panels per regular step, powerURV (2q+1) n-wide QRs."""
+    return 2 * b * (-(-n // b) - 1) + (2 * q + 1) * n
+
+
+def kernel_entries(prof, step_s, n, b, q, sweeps):
+    """Per-kernel figures of the non-GEMM kernels (panel QR
+    algorithmic GB/s and us/column, Jacobi ms/call and sweeps, split-K share)."""
+    pq, jr, jf, sk = prof["panel_qr"], prof["jacobi_rounds"], prof["jacobi_finish"], prof["splitk_reduce"]
+    cols = _panel_columns(n, b, q)
+    out = {
+        "panel_qr": {"ms_per_step": pq["ms"], "launches": pq["count"],
+                     "us_per_column": 1e3 * pq["ms"] / cols if cols else None,
+                     "algorithmic_GBps": pq["bytes"] / (pq["ms"] / 1e3) / 1e9 if pq["ms"] else None,
+                     "bytes_model": "8*3*rows*cols per panel (read A, write R and Y)",
+                     "share_of_step": pq["ms"] / 1e3 / step_s},
+        "jacobi": {"ms_per_step": jr["ms"] + jf["ms"], "calls": jr["count"],
+                   "ms_per_call": (jr["ms"] + jf["ms"]) / max(jr["count"], 1),
+                   "sweeps_mean": float(np.mean(sweeps)) if len(sweeps) else None,
+                   "sweeps_max": int(np.max(sweeps)) if len(sweeps) else None},
+        "splitk_reduce": {"ms_per_step": sk["ms"], "launches": sk["count"],
+                          "share_of_step": sk["ms"] / 1e3 / step_s},
+    }
+    return out
+
+
+def run_ours(args, nested=False):
+    import torch
+    ws, rank, local = dist_env()
+    _init_dist(ws, local)
     import paper_2106_13402_b200 as pk
     import paper_2106_13402_b200.device as dv
     from paper_2106_13402_b200 import _lib
-    from paper_2106_13402_b200._lib import deye, dempty
+    from paper_2106_13402_b200._lib import dempty
 
     n, b, q = args.n, args.b, args.q
+    steps, warmup = (1, 1) if nested else (args.steps, args.warmup)
     A = make_decay_matrix(n, seed=30 + rank)
     # Gaussian samples exactly as the reference draws them (host PCG64)
     rng = pk.RngStream(3)
@@ -265,33 +454,26 @@ def run_ours(args):
     T = dempty(n, n)
     U = dempty(n, n)
     V = dempty(n, n)
-    eye_idx = torch.arange(n, device="cuda")
+
+    def rutv_step():
+        _lib_copy(A, T)                 # randUTV works in place on T (randutv.py:114)
+        _lib_eye(U)
+        _lib_eye(V)
+        rrun.run(T, U, V, Gr)
 
     def step():
-        T.t.copy_(A.t)
-        U.t.zero_()
-        U.t[eye_idx, eye_idx] = 1.0
-        V.t.zero_()
-        V.t[eye_idx, eye_idx] = 1.0
-        rrun.run(T, U, V, Gr)
+        rutv_step()
         prun.run(A, Gp)
 
-    def sync_all():
-        torch.cuda.synchronize()
-        if ws > 1:
-            torch.distributed.barrier()
-            torch.cuda.synchronize()
-
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
-    sync_all()
+    _sync_all(ws)
 
     # per-algorithm split (untimed) + roofline inputs of the dominant kernel
     e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
     _lib.profile_begin()
     e0.record()
-    T.t.copy_(A.t); U.t.zero_(); U.t[eye_idx, eye_idx] = 1.0; V.t.zero_(); V.t[eye_idx, eye_idx] = 1.0
-    rrun.run(T, U, V, Gr)
+    rutv_step()
     e1.record()
     prun.run(A, Gp)
     e2.record()
@@ -299,27 +481,23 @@ def run_ours(args):
     rutv_s = e0.elapsed_time(e1) / 1e3
     purv_s = e1.elapsed_time(e2) / 1e3
     sweeps = rrun.status.cpu().numpy()
-    sync_all()
+    _sync_all(ws)
 
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.5)
-    sync_all()
+    _sync_all(ws)
     launches0 = _lib.launch_count()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record()
-    for _ in range(args.steps):
+    for _ in range(steps):
         step()
     t1.record()
-    sync_all()
+    _sync_all(ws)
     launches = _lib.launch_count() - launches0
     clk = clocks.stop()
-    secs = t0.elapsed_time(t1) / 1e3
-    if ws > 1:
-        tt = torch.tensor([secs], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        secs = float(tt.item())
-    per_step = secs / args.steps
+    secs = _max_over_ranks(ws, t0.elapsed_time(t1) / 1e3)
+    per_step = secs / steps
     f_rutv = randutv_flops(n, n, b, q)
     f_purv = powerurv_flops(n, n, q)
     flops = f_rutv + f_purv
@@ -327,7 +505,7 @@ def run_ours(args):
 
     # ---- e2e through the public API (host numpy in, host numpy out) ----
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not nested:
         a_host = A.to_numpy()
         a_host = np.asfortranarray(a_host)
         del T, U, V
@@ -341,16 +519,12 @@ def run_ours(args):
         # in the caching allocator), then E2E_STEPS timed calls, wall clock
         e2e_step()
         torch.cuda.synchronize()
-        e2e_steps = max(1, min(args.steps, 2))
+        e2e_steps = max(1, min(steps, 2))
         te = time.perf_counter()
         for _ in range(e2e_steps):
             e2e_step()
         torch.cuda.synchronize()
-        e2e_s = (time.perf_counter() - te) / e2e_steps
-        if ws > 1:
-            tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-            e2e_s = float(tt.item())
+        e2e_s = _max_over_ranks(ws, (time.perf_counter() - te) / e2e_steps)
         h2d = 8 * (2 * n * n + sum(k * b for k in range(n, b, -b)) + n * n)
         d2h = 8 * (3 * n * n + 5 * n * n) + 8 * (-(-n // b)) * 2
         e2e = {"value": ws * flops / e2e_s / 1e12, "unit": "TFLOP/s", "seconds": e2e_s,
@@ -367,19 +541,22 @@ def run_ours(args):
     gemm_tflops = g["flops"] / gemm_busy_s / 1e12 if gemm_busy_s > 0 else 0.0
     phase = {k: round(v["ms"], 3) for k, v in prof.items()}
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and ws == 1 and not args.no_cpu and not nested:
         r = cpu_sample_run()
         cpu = {"value": r["flops"] / r["seconds"] / 1e12, "unit": "TFLOP/s", "cores": cpu_threads(),
-               "kind": "port", "sample": r["sample"], "seconds": r["seconds"]}
+               "kind": r["kind"], "sample": r["sample"], "seconds": r["seconds"]}
     line = {
-        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": steps,
+        "warmup": warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (device-generated Gaussian-decay A; G from the reference PCG64 stream)",
-        "config": config_dict(args),
+        "config": config_dict(args, ws),
         "seconds": {"randutv": rutv_s, "powerurv": purv_s, "step": per_step},
         "tflops": {"randutv": f_rutv / rutv_s / 1e12, "powerurv": f_purv / purv_s / 1e12,
-                   "frac_of_fp64_peak": value / ws / FP64_PEAK_TFLOPS},
+                   "algorithmic_over_peak": value / ws / FP64_PEAK_TFLOPS,
+                   "note": "algorithmic_over_peak divides SURVEY §8d FLOPs (powerURV executes "
+                           "~8n^3/3 fewer per round, csrc/powerurv.cu) by the peak; it is not a "
+                           "utilisation figure - roofline.frac is"},
         "roofline": {"bound": "tensor", "kernel": "dgemm_tma_kernel (DMMA.8x8x4)",
                      "achieved": gemm_tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": gemm_tflops / FP64_PEAK_TFLOPS, "traffic": GEMM_TRAFFIC["bytes"],
@@ -390,6 +567,7 @@ def run_ours(args):
                                         "intervals over all streams (CUDA events, live)",
                      "sum_of_launch_ms": g["ms"],
                      "launches_per_step": g["count"]},
+        "kernels": kernel_entries(prof, rutv_s + purv_s, n, b, q, sweeps),
         "phase_ms": phase,
         "jacobi_sweeps": {"mean": float(np.mean(sweeps)), "max": int(np.max(sweeps))},
         "gpu_launches": int(launches),
@@ -397,11 +575,79 @@ def run_ours(args):
         "e2e": e2e,
         "cpu_baseline": cpu,
     }
+    del A, Gr, Gp, rrun, prun
+    torch.cuda.empty_cache()
+    if nested:
+        return line
+    if ws == 1 and not args.no_c4:
+        line["c4"] = run_c4(args, nested=True)        # the 1-GPU base of the C4 scaling curve
     if rank == 0:
         print(json.dumps(line), flush=True)
+    _finish_dist(ws)
+
+
+def _finish_dist(ws):
     if ws > 1:
+        import torch
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# C2: powerURV q=2 on 8192^2 (BASELINE configs[1])
+# ---------------------------------------------------------------------------
+
+C2_METRIC = "powerURV q=2 fp64 8192^2: FP64 TFLOP/s (algorithmic, SURVEY §8d)"
+
+
+def run_c2(args):
+    import torch
+    ws, rank, local = dist_env()
+    _init_dist(ws, local)
+    import paper_2106_13402_b200 as pk
+    import paper_2106_13402_b200.device as dv
+    from paper_2106_13402_b200 import _lib
+    n, q = 8192, 2
+    A = make_decay_matrix(n, seed=20 + rank)
+    Gp = _lib.dfrom_numpy(pk.gaussian(n, n, pk.RngStream(2)))
+    prun = dv.PowerUrvRun(n, n, q)
+    for _ in range(args.warmup):
+        prun.run(A, Gp)
+    _sync_all(ws)
+    _lib.profile_begin()
+    prun.run(A, Gp)
+    prof = _lib.profile_end()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = _lib.launch_count()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(args.steps):
+        prun.run(A, Gp)
+    t1.record()
+    _sync_all(ws)
+    clk = clocks.stop()
+    launches = _lib.launch_count() - launches0
+    per = _max_over_ranks(ws, t0.elapsed_time(t1) / 1e3) / args.steps
+    flops = powerurv_flops(n, n, q)
+    g = prof["dgemm_dmma"]
+    gb = (g["busy_ms"] or g["ms"]) / 1e3
+    line = {"metric": C2_METRIC, "value": ws * flops / per / 1e12, "unit": "TFLOP/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (device-generated Gaussian-decay A, seed 20; G = RngStream(2))",
+            "config": {"workload": f"C2 powerURV q={q} on {n}x{n} fp64",
+                       "l2_policy": "inputs (512 MiB) larger than the 126 MB L2; no explicit flush",
+                       "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
+            "roofline": {"bound": "tensor", "kernel": "dgemm_tma_kernel (DMMA.8x8x4)",
+                         "achieved": g["flops"] / gb / 1e12 if gb else 0.0, "peak": FP64_PEAK_TFLOPS,
+                         "unit": "TFLOP/s", "frac": g["flops"] / gb / 1e12 / FP64_PEAK_TFLOPS if gb else 0.0,
+                         "traffic": None, "share_of_step": gb / per},
+            "phase_ms": {k: round(v["ms"], 3) for k, v in prof.items()},
+            "gpu_launches": int(launches), "clocks": clk, "e2e": None, "cpu_baseline": None}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    _finish_dist(ws)
 
 
 # ---------------------------------------------------------------------------
@@ -411,21 +657,19 @@ def run_ours(args):
 C4_METRIC = "row-sharded powerURV q=1, 524288x4096 fp64: FP64 TFLOP/s (algorithmic, SURVEY §8d)"
 
 
-def run_c4(args):
+def run_c4(args, nested=False):
+    """C4 through the product path: utv_powerurv_sharded_f64 on every rank
+    (collectives inside libutvb200: NCCL over the ranks' GPUs at N > 1)."""
     import torch
     ws, rank, local = dist_env()
+    _init_dist(ws, local)
     from paper_2106_13402_b200 import sharded
     import paper_2106_13402_b200 as pk
     from paper_2106_13402_b200 import _lib
     from paper_2106_13402_b200._lib import dempty
-    if ws > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        comm = sharded.TorchComm()
-    else:
-        comm = sharded.Comm()
+    comm = sharded.NativeComm.nccl() if ws > 1 else sharded.NativeComm.local_group(1)[0]
     m, n, q = args.c4_rows, args.c4_cols, 1
+    steps, warmup = (1, 1) if nested else (args.steps, args.warmup)
     rows = [m // ws + (1 if r < m % ws else 0) for r in range(ws)]
     gen = torch.Generator(device="cuda").manual_seed(40 + rank)
     a = dempty(rows[rank], n)
@@ -434,51 +678,48 @@ def run_c4(args):
     torch.cuda.synchronize()
 
     def step():
-        return sharded.power_urv_sharded(a, g, q, comm)
+        return sharded.power_urv_sharded_native(a, g, q, comm)
 
-    def sync_all():
-        torch.cuda.synchronize()
-        if ws > 1:
-            torch.distributed.barrier()
-            torch.cuda.synchronize()
-
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         out = step()
         del out
-    sync_all()
+    _sync_all(ws)
     clocks = ClockSampler(local)
     clocks.start()
     launches0 = _lib.launch_count()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record()
-    for _ in range(args.steps):
+    for _ in range(steps):
         out = step()
         del out
     t1.record()
-    sync_all()
+    _sync_all(ws)
     clk = clocks.stop()
     launches = _lib.launch_count() - launches0
-    secs = t0.elapsed_time(t1) / 1e3
-    if ws > 1:
-        tt = torch.tensor([secs], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        secs = float(tt.item())
-    per = secs / args.steps
+    per = _max_over_ranks(ws, t0.elapsed_time(t1) / 1e3) / steps
     flops = powerurv_flops(m, n, q)
     line = {"metric": C4_METRIC, "value": flops / per / 1e12, "unit": "TFLOP/s", "n_gpus": ws,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
+            "steps": steps, "warmup": warmup, "ms_per_step": per * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (device N(0,1) rows per rank; G from the reference PCG64 stream)",
             "config": {"workload": f"C4 powerURV q={q} on {m}x{n} fp64, row-sharded over {ws} rank(s)",
-                       "rows_per_rank": rows, "parallelism": f"row shards x{ws} (NCCL allreduce + TSQR)",
+                       "rows_per_rank": rows,
+                       "parallelism": f"row shards x{ws} (utv_powerurv_sharded_f64: NCCL allgather "
+                                      f"+ allreduce + broadcast inside libutvb200)" if ws > 1
+                                      else "1 GPU (utv_powerurv_sharded_f64, 1-rank communicator)",
                        "l2_policy": "inputs (16 GiB / ranks) larger than L2"},
             "frac_of_fp64_peak": flops / per / 1e12 / ws / FP64_PEAK_TFLOPS,
             "gpu_launches": int(launches), "clocks": clk, "e2e": None, "cpu_baseline": None}
+    comm.close()
+    del a, g
+    torch.cuda.empty_cache()
+    if nested:
+        return line
+    if ws > 1 and not args.no_replicas:
+        line["headline_replicas"] = run_ours(args, nested=True)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if ws > 1:
-        torch.distributed.barrier()
-        torch.distributed.destroy_process_group()
+    _finish_dist(ws)
 
 
 # ---------------------------------------------------------------------------
@@ -535,12 +776,16 @@ def run_c5(args):
     run = dv.RandUtvRun32(n, n, b, q)
     T = dempty(n, n, dtype=torch.float32)
     U, V = _eye32(n), _eye32(n)
-    idx = torch.arange(n, device="cuda")
+    lib = _lib.load()
+
+    def eye32(m):
+        _lib.check(lib.utv_slaset(b"A", m.rows, m.cols, 0.0, 1.0, m.ptr, m.ld, _lib.stream_ptr()),
+                   "utv_slaset")
 
     def step():
         T.t.copy_(A.t)
-        U.t.zero_(); U.t[idx, idx] = 1.0
-        V.t.zero_(); V.t[idx, idx] = 1.0
+        eye32(U)
+        eye32(V)
         run.run(T, U, V, G)
 
     for _ in range(args.warmup):
@@ -587,6 +832,21 @@ def run_c5(args):
         torch.distributed.destroy_process_group()
 
 
+def _spawn_ranks(n):
+    """--gpus N > 1 outside torchrun: re-launch this script as N ranks."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -598,8 +858,12 @@ def main():
     ap.add_argument("--q", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--workload", choices=["headline", "c4", "c5"], default="headline",
-                    help="headline = BASELINE metric (n=16384 powerURV + randUTV); "
+    ap.add_argument("--no-c4", action="store_true", help="N=1: skip the nested 1-GPU C4 run")
+    ap.add_argument("--no-replicas", action="store_true", help="N>1: skip the nested headline replicas")
+    ap.add_argument("--workload", choices=["auto", "headline", "c2", "c4", "c5"], default="auto",
+                    help="auto = headline at N=1, row-sharded C4 at N>1; "
+                         "headline = BASELINE metric (n=16384 powerURV + randUTV); "
+                         "c2 = powerURV q=2 8192^2 (BASELINE configs[1]); "
                          "c4 = row-sharded tall powerURV (BASELINE configs[3]); "
                          "c5 = fp32 3xTF32 randUTV (BASELINE configs[4])")
     ap.add_argument("--c5-n", type=int, default=32768)
@@ -607,12 +871,19 @@ def main():
     ap.add_argument("--c4-rows", type=int, default=524288)
     ap.add_argument("--c4-cols", type=int, default=4096)
     args = ap.parse_args()
-    if args.workload == "c4" and args.impl != "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_spawn_ranks(args.gpus))
+    os.environ.setdefault("NCCL_DEBUG", "INFO")       # rank count visible in the NCCL log
+    ws = dist_env()[0]
+    wl = args.workload if args.workload != "auto" else ("headline" if ws == 1 else "c4")
+    if args.impl == "reference":
+        run_reference(args, wl)
+    elif wl == "c4":
         run_c4(args)
-    elif args.workload == "c5" and args.impl != "reference":
+    elif wl == "c5":
         run_c5(args)
-    elif args.impl == "reference":
-        run_reference(args)
+    elif wl == "c2":
+        run_c2(args)
     else:
         run_ours(args)
 

@@ -108,6 +108,12 @@ int utv_dlaset(char uplo, int m, int n, double alpha, double beta, double* A, lo
                void* stream);
 int utv_ddiag_scale(char side, int m, int n, const double* d, double alpha, double* A, long lda,
                     void* stream);
+/* FP32 dlaset (identity / zero initialisation of the fp32 randUTV's U, V). */
+int utv_slaset(char uplo, int m, int n, float alpha, float beta, float* A, long lda, void* stream);
+/* *flag (device int) <- 1 if any entry of the m x n block is NaN or +-Inf,
+ * else 0: the finite test of check_matrix (matrix.py:36-49) on an uploaded
+ * copy, so the public API raises ValueError before any RNG draw. */
+int utv_dnonfinite(int m, int n, const double* A, long lda, int* flag, void* stream);
 /* B (n x m) = A^T (A is m x n).  Used to take a C-order host draw (the
  * reference's gaussian() before its np.asfortranarray copy, matrix.py:52-60)
  * to column-major on the device instead of transposing 2 GiB on the host. */
@@ -215,6 +221,59 @@ int utv_powerurv_f64_yhat(int m, int n, int q, const double* A, long lda, const 
                           long ldy0, double* Uy, long lduy, double* Ut, long ldut, double* R,
                           long ldr, double* Vy, long ldvy, double* Vt, long ldvt, void* work,
                           size_t lwork, void* stream, void* vq_ready, void* r_ready);
+
+/* ---- Row-sharded powerURV over several GPUs (BASELINE C4) ----
+ * The reference has no multi-GPU path (powerurv.py:41-72 is one process);
+ * this is its SPMD form: one process (or, for emulation, one host thread)
+ * per rank, rank i owning the row block A_i (m_i x n, m_i >= n) and the
+ * same n x n G.  Collectives run on the caller's stream through a
+ * utv_comm_t: NCCL (libnccl is dlopen'ed, the process's loaded copy
+ * preferred; UTV_NCCL_LIB overrides) or an in-process local group of P
+ * ranks (threads; device-to-device copies + a host barrier; rank-order
+ * sums).  Per power round: local GEMM, TSQR (allgather of n x n R's),
+ * local GEMM + allreduce of the n x n Y, redundant hqr_full(Y); final TSQR
+ * + Householder reconstruction (rank 0 factors the top n x n block and
+ * broadcasts it; every rank solves for its own rows).
+ *
+ * utv_comm_nccl_unique_id: 128-byte ncclUniqueId (rank 0; ship it to the
+ *   other ranks out of band, e.g. torch.distributed.broadcast_object_list).
+ * utv_comm_init_nccl: collective over all ranks; binds the current device.
+ * utv_comm_from_nccl: borrow an existing ncclComm_t (not destroyed).
+ * utv_comm_init_local: nranks handles of one in-process group (comms[r] is
+ *   rank r; drive each from its own host thread and stream).
+ * Returns -1004 (UTV_ERR_COMM) when NCCL is unavailable or a collective fails. */
+typedef struct utv_comm_s utv_comm_s;
+typedef utv_comm_s* utv_comm_t;
+int utv_comm_nccl_available(void);
+int utv_comm_nccl_unique_id(void* id128);
+int utv_comm_init_nccl(const void* id128, int nranks, int rank, utv_comm_t* comm);
+int utv_comm_from_nccl(void* nccl_comm, utv_comm_t* comm);
+int utv_comm_init_local(int nranks, utv_comm_t* comms);
+int utv_comm_rank(const utv_comm_s* comm);
+int utv_comm_size(const utv_comm_s* comm);
+int utv_comm_destroy(utv_comm_t comm);
+/* The three collectives of the sharded path, exposed for tests: in-place
+ * sum; recv = rank-ordered concatenation of count doubles each; in place. */
+int utv_comm_allreduce_sum_f64(utv_comm_t comm, double* buf, size_t count, void* stream);
+int utv_comm_allgather_f64(utv_comm_t comm, const double* send, double* recv, size_t count,
+                           void* stream);
+int utv_comm_broadcast_f64(utv_comm_t comm, double* buf, size_t count, int root, void* stream);
+
+/* Row-sharded power_urv_from_sample (powerurv.py:41-72), SPMD: every rank
+ * calls with its m_local rows of A, the same n, q and G.  Outputs: this
+ * rank's rows of Uq.Y (Uy, m_local x n) and the replicated Uq.Twy (Ut),
+ * R (n x n; rows n.. of the reference's m x n R are zero), Vq.Y (Vy) and
+ * Vq.Twy (Vt), all n x n.  chunk_rows (<= 0: the panel-QR limit,
+ * utv_dgeqrf_rows_max) caps the local TSQR leaves.  The ranks first agree
+ * on (n, q, argument validity) with one 4-double allreduce and a stream
+ * synchronisation; a rank with an invalid argument returns its own code,
+ * the others -1004.  The Householder reconstruction does not reproduce
+ * hqr_full's skip rule (tau = 0) for exactly dependent columns. */
+size_t utv_powerurv_sharded_bufsize(int m_local, int n, int nranks, int chunk_rows);
+int utv_powerurv_sharded_f64(utv_comm_t comm, int m_local, int n, int q, const double* A, long lda,
+                             const double* G, long ldg, double* Uy, long lduy, double* Ut,
+                             long ldut, double* R, long ldr, double* Vy, long ldvy, double* Vt,
+                             long ldvt, int chunk_rows, void* work, size_t lwork, void* stream);
 
 /* Instrumentation (no reference counterpart).
  * utv_launch_count: number of libutvb200 kernel launches since load.

@@ -174,6 +174,33 @@ def power_urv(a, q, g):
 
 
 # ---------------------------------------------------------------------------
+# randomized SVD cross-check (rsvd.py:31-78; SPEC acceptance 2)
+# ---------------------------------------------------------------------------
+
+def rsvd(a, g_shared, ell, q):
+    """Rank-ell randomized SVD from the first ell columns of G: thin QR between
+    every application of A and A^T (rsvd.py:56-63), then the small SVD of
+    Q^T A lifted back (rsvd.py:65-67).  Returns (U_rsvd, sigma, V)."""
+    a = np.asarray(a, dtype=np.float64)
+
+    def thin_q(x):                                   # hqr_thin (qr.py:134-138)
+        y, t, _ = householder_qr(x)
+        return wy_materialize(y, t, x.shape[1])
+
+    basis = thin_q(a @ g_shared[:, :ell])
+    for _ in range(q):
+        basis = thin_q(a @ thin_q(a.T @ basis))
+    u_s, s, v = svd_signed(basis.T @ a, full=False)
+    return basis @ u_s, s, v
+
+
+def projector_gap(u1, u2, a):
+    """||u1 u1^T a - u2 u2^T a||_F / ||a||_F (rsvd.py:81-98)."""
+    d = u1 @ (u1.T @ a) - u2 @ (u2.T @ a)
+    return float(np.linalg.norm(d) / np.linalg.norm(a))
+
+
+# ---------------------------------------------------------------------------
 # randUTV basic (randutv.py:110-193, 228-235)
 # ---------------------------------------------------------------------------
 

@@ -11,12 +11,12 @@ from .powerurv import UrvFactorization, power_urv, power_urv_from_sample, rurv
 from .qr import PivotedQr, QFactor, apply_q, hqr_full, hqr_thin, hqrcp, materialize_q
 from .randutv import (ErrorTracker, UtvFactorization, error_update, randutv_basic,
                       randutv_boosted, randutv_partial)
-from .svd import SvdTriple, svd_dense
+from .svd import SvdTriple, svd_dense, svd_tall_thin_left
 
 __all__ = [
     "MACHINE_EPS", "RngStream", "gaussian", "frobenius_norm", "check_matrix",
     "QFactor", "PivotedQr", "hqr_full", "hqr_thin", "hqrcp", "apply_q", "materialize_q",
-    "SvdTriple", "svd_dense",
+    "SvdTriple", "svd_dense", "svd_tall_thin_left",
     "UrvFactorization", "power_urv", "power_urv_from_sample", "rurv",
     "UtvFactorization", "ErrorTracker", "error_update", "randutv_basic",
     "randutv_boosted", "randutv_partial",

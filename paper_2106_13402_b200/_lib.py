@@ -81,6 +81,9 @@ SIGNATURES = {
                                  c_void_p, c_long, ctypes.c_float, c_void_p, c_long, c_void_p]),
     "utv_dlacpy": (c_int, [c_int, c_int, c_void_p, c_long, c_void_p, c_long, c_void_p]),
     "utv_dlaset": (c_int, [c_char, c_int, c_int, c_double, c_double, c_void_p, c_long, c_void_p]),
+    "utv_slaset": (c_int, [c_char, c_int, c_int, ctypes.c_float, ctypes.c_float, c_void_p, c_long,
+                           c_void_p]),
+    "utv_dnonfinite": (c_int, [c_int, c_int, c_void_p, c_long, c_void_p, c_void_p]),
     "utv_dtri_zero": (c_int, [c_char, c_int, c_int, c_void_p, c_long, c_void_p]),
     "utv_dtranspose": (c_int, [c_int, c_int, c_void_p, c_long, c_void_p, c_long, c_void_p]),
     "utv_dgen_bie": (c_int, [c_int, c_void_p, c_long, c_void_p]),
@@ -96,6 +99,22 @@ SIGNATURES = {
     "utv_dtrsm_bufsize": (c_size_t, [c_int, c_int]),
     "utv_dtrsm_right": (c_int, [c_char, c_char, c_char, c_int, c_int, c_void_p, c_long, c_void_p,
                                 c_long, c_void_p, c_size_t, c_void_p]),
+    "utv_comm_nccl_available": (c_int, []),
+    "utv_comm_nccl_unique_id": (c_int, [c_void_p]),
+    "utv_comm_init_nccl": (c_int, [c_void_p, c_int, c_int, c_void_p]),
+    "utv_comm_from_nccl": (c_int, [c_void_p, c_void_p]),
+    "utv_comm_init_local": (c_int, [c_int, c_void_p]),
+    "utv_comm_rank": (c_int, [c_void_p]),
+    "utv_comm_size": (c_int, [c_void_p]),
+    "utv_comm_destroy": (c_int, [c_void_p]),
+    "utv_comm_allreduce_sum_f64": (c_int, [c_void_p, c_void_p, c_size_t, c_void_p]),
+    "utv_comm_allgather_f64": (c_int, [c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "utv_comm_broadcast_f64": (c_int, [c_void_p, c_void_p, c_size_t, c_int, c_void_p]),
+    "utv_powerurv_sharded_bufsize": (c_size_t, [c_int, c_int, c_int, c_int]),
+    "utv_powerurv_sharded_f64": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_long, c_void_p,
+                                         c_long, c_void_p, c_long, c_void_p, c_long, c_void_p,
+                                         c_long, c_void_p, c_long, c_void_p, c_long, c_int,
+                                         c_void_p, c_size_t, c_void_p]),
     "utv_launch_count": (ctypes.c_longlong, []),
     "utv_profile_begin": (None, []),
     "utv_profile_end": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
@@ -430,18 +449,18 @@ def dempty(rows, cols, ld=None, dtype=None):
     return DMat(t, rows, cols, ld)
 
 
-def dzeros(rows, cols):
-    m = dempty(rows, cols)
-    m.t.zero_()
+def _laset(m, alpha, beta):
+    check(load().utv_dlaset(b"A", m.rows, m.cols, alpha, beta, m.ptr, m.ld, stream_ptr()),
+          "utv_dlaset")
     return m
+
+
+def dzeros(rows, cols):
+    return _laset(dempty(rows, cols), 0.0, 0.0)
 
 
 def deye(n):
-    torch = torch_cuda()
-    m = dzeros(n, n)
-    idx = torch.arange(n, device="cuda")
-    m.t[idx, idx] = 1.0
-    return m
+    return _laset(dempty(n, n), 0.0, 1.0)
 
 
 def dfrom_numpy(a, pinned=False, dtype=None):

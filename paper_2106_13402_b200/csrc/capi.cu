@@ -21,6 +21,9 @@ int randutv_basic_f32(int m, int n, int b, int q, float* Tp, long ldt, float* Up
                       float* Vp, long ldv, const float* G, long ldg, double* errsq, double* trail2,
                       int* svd_status, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t powerurv_ws_doubles(int m, int n);
+size_t powerurv_sharded_ws_doubles(int m, int n, int nranks, int cap);
+int powerurv_sharded(Comm* comm, int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy,
+                     Mat Vt, int cap, double* ws, size_t ws_doubles, cudaStream_t st);
 int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, Mat Vt, double* ws,
              size_t ws_doubles, cudaStream_t st, cudaEvent_t vq_ready, const double* yhat0 = nullptr,
              long ldy0 = 0, cudaEvent_t r_ready = nullptr);
@@ -215,6 +218,27 @@ int utv_dlaset(char uplo, int m, int n, double alpha, double beta, double* A, lo
   return laset(u, m, n, alpha, beta, A, lda, S(stream));
 }
 
+int utv_slaset(char uplo, int m, int n, float alpha, float beta, float* A, long lda,
+               void* stream) {
+  int u;
+  if (uplo == 'U' || uplo == 'u') u = 1;
+  else if (uplo == 'L' || uplo == 'l') u = 2;
+  else if (uplo == 'A' || uplo == 'a') u = 0;
+  else return -1;
+  if (m < 0) return -2;
+  if (n < 0) return -3;
+  if (lda < m) return -7;
+  return laset_f32(u, m, n, alpha, beta, A, lda, S(stream));
+}
+
+int utv_dnonfinite(int m, int n, const double* A, long lda, int* flag, void* stream) {
+  if (m < 0) return -1;
+  if (n < 0) return -2;
+  if (lda < m) return -4;
+  if (!flag) return -5;
+  return nonfinite(A, lda, m, n, flag, S(stream));
+}
+
 int utv_dtranspose(int m, int n, const double* A, long lda, double* Bm, long ldb, void* stream) {
   if (m < 0) return -1;
   if (n < 0) return -2;
@@ -394,6 +418,33 @@ int utv_powerurv_f64_yhat(int m, int n, int q, const double* A, long lda, const 
                   Mat{Uy, lduy, m, n}, Mat{Ut, ldut, n, n}, Mat{R, ldr, m, n}, Mat{Vy, ldvy, n, n},
                   Mat{Vt, ldvt, n, n}, (double*)work, lwork / sizeof(double), S(stream),
                   (cudaEvent_t)vq_ready, Yhat0, ldy0, (cudaEvent_t)r_ready);
+}
+
+size_t utv_powerurv_sharded_bufsize(int m_local, int n, int nranks, int chunk_rows) {
+  return B(powerurv_sharded_ws_doubles(m_local, n, nranks < 1 ? 1 : nranks, chunk_rows));
+}
+
+int utv_powerurv_sharded_f64(utv_comm_t comm, int m_local, int n, int q, const double* A, long lda,
+                             const double* G, long ldg, double* Uy, long lduy, double* Ut,
+                             long ldut, double* R, long ldr, double* Vy, long ldvy, double* Vt,
+                             long ldvt, int chunk_rows, void* work, size_t lwork, void* stream) {
+  if (!comm) return -1;
+  // argument errors are reported after the ranks agree (see powerurv_sharded)
+  int bad = 0;
+  if (!ld_ok(lda, m_local)) bad = -6;
+  else if (!ld_ok(ldg, n)) bad = -8;
+  else if (!ld_ok(lduy, m_local)) bad = -10;
+  else if (!ld_ok(ldut, n)) bad = -12;
+  else if (!ld_ok(ldr, n)) bad = -14;
+  else if (!ld_ok(ldvy, n)) bad = -16;
+  else if (!ld_ok(ldvt, n)) bad = -18;
+  if (bad) m_local = -1;  // forces the agreed failure path
+  const int rc = powerurv_sharded((Comm*)comm, m_local, n, q, Mat{(double*)A, lda, m_local, n},
+                                  Mat{(double*)G, ldg, n, n}, Mat{Uy, lduy, m_local, n},
+                                  Mat{Ut, ldut, n, n}, Mat{R, ldr, n, n}, Mat{Vy, ldvy, n, n},
+                                  Mat{Vt, ldvt, n, n}, chunk_rows, (double*)work,
+                                  lwork / sizeof(double), S(stream));
+  return bad ? bad : rc;
 }
 
 }  // extern "C"

@@ -17,6 +17,8 @@ enum : int {
   UTV_ERR_CUDA = -1000,      // a CUDA runtime call failed
   UTV_ERR_WORKSPACE = -1001, // workspace too small
   UTV_ERR_ALIGN = -1002,     // leading dimension not even / pointer not 8-byte aligned
+  UTV_ERR_DEVICE = -1003,    // called on a different device than the one the library bound to
+  UTV_ERR_COMM = -1004,      // a collective failed (NCCL missing / error) or ranks disagree
   UTV_ERR_NOCONV = 1,        // Jacobi SVD did not converge within the sweep cap
 };
 

@@ -106,8 +106,8 @@ __global__ void copy_kernel(const double* __restrict__ S, long lds, double* __re
 // LAPACK dlaset semantics: uplo 0 = whole, 1 = strictly upper + diag,
 // 2 = strictly lower + diag; off-diagonal entries <- alpha, diagonal <- beta.
 // uplo 3 / 4: strictly upper / lower part only (diagonal untouched).
-__global__ void laset_kernel(double* A, long lda, int rows, int cols, int uplo, double alpha,
-                             double beta) {
+template <typename F>
+__global__ void laset_kernel(F* A, long lda, int rows, int cols, int uplo, F alpha, F beta) {
   const long total = (long)rows * cols;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total;
        i += (long)gridDim.x * blockDim.x) {
@@ -116,6 +116,19 @@ __global__ void laset_kernel(double* A, long lda, int rows, int cols, int uplo, 
     else if (uplo == 3 ? r < c : (uplo == 4 ? r > c : false)) A[r + (long)c * lda] = alpha;
     else if (uplo == 0 || (uplo == 1 && r < c) || (uplo == 2 && r > c)) A[r + (long)c * lda] = alpha;
   }
+}
+
+// *flag <- 1 if any entry of the block is NaN or +-Inf (flag zeroed by the
+// caller); the finite half of check_matrix (matrix.py:36-49) on the device.
+__global__ void nonfinite_kernel(const double* A, long lda, int rows, int cols, int* flag) {
+  const long total = (long)rows * cols;
+  int bad = 0;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total;
+       i += (long)gridDim.x * blockDim.x) {
+    const int r = (int)(i % rows), c = (int)(i / rows);
+    bad |= !isfinite(A[r + (long)c * lda]);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
 // A <- alpha * diag(d) A (rows, side 0) or alpha * A diag(d) (cols, side 1).
@@ -239,6 +252,27 @@ int laset(int uplo, int rows, int cols, double alpha, double beta, double* A, lo
   ProfScope ps(PROF_OPS, 0.0, 8.0 * rows * cols, st);
   ops::laset_kernel<<<ops::grid_for((long)rows * cols), 256, 0, st>>>(A, lda, rows, cols, uplo,
                                                                       alpha, beta);
+  UTV_CUDA(cudaGetLastError());
+  return UTV_OK;
+}
+
+int laset_f32(int uplo, int rows, int cols, float alpha, float beta, float* A, long lda,
+              cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return UTV_OK;
+  ProfScope ps(PROF_OPS, 0.0, 4.0 * rows * cols, st);
+  ops::laset_kernel<<<ops::grid_for((long)rows * cols), 256, 0, st>>>(A, lda, rows, cols, uplo,
+                                                                      alpha, beta);
+  UTV_CUDA(cudaGetLastError());
+  return UTV_OK;
+}
+
+int nonfinite(const double* A, long lda, int rows, int cols, int* flag, cudaStream_t st) {
+  UTV_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+  if (rows <= 0 || cols <= 0) return UTV_OK;
+  ProfScope ps(PROF_OPS, 0.0, 8.0 * rows * cols, st);
+  const long cap = 8L * num_sms();
+  const long g = std::min<long>(cap, ((long)rows * cols + 255) / 256);
+  ops::nonfinite_kernel<<<(int)std::max<long>(g, 1), 256, 0, st>>>(A, lda, rows, cols, flag);
   UTV_CUDA(cudaGetLastError());
   return UTV_OK;
 }

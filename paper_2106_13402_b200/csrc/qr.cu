@@ -84,6 +84,10 @@ int orgqr(Mat Y, Mat T, Mat Q, double* ws, size_t ws_doubles, cudaStream_t st) {
 // K3/K4: blocked Householder QR.
 // ---------------------------------------------------------------------------
 size_t geqrf_ws_doubles(int rows, int cols, bool /*want_t*/) {
+  // taller than the fused panel kernel accepts: TSQR + reconstruction (tsqr.cu)
+  if (rows > panel_rows_max())
+    return 4096 + tsqr_ws_doubles(rows, cols, 1, panel_rows_max()) +
+           (size_t)round_up(cols, 4) * cols + reconstruct_ws_doubles(cols);
   // fused panel QR scratch + merge temporaries + trailing larfb workspace
   return 4096 + sumsq_scratch_doubles() + panel_ws_doubles() +
          2 * (size_t)round_up(cols, 4) * qr::PANEL + larfb_ws_doubles(rows, cols, qr::PANEL);
@@ -222,13 +226,36 @@ int build_t(Mat Y, Mat T, double* ws, size_t ws_doubles, cudaStream_t st) {
   return UTV_OK;
 }
 
+// Panels taller than the fused kernel's row limit (148 slabs of <= 512 rows):
+// TSQR over row chunks on this GPU, then the Householder reconstruction
+// (tsqr.cu) so that Y, the dense forward Tw and R = S R_tsqr are hqr_full's
+// (qr.py:71-100) up to roundoff for full-rank input.  The skip rule
+// (tau = 0 for an exactly dependent column) is not reproduced on this path.
+static int geqrf_tall(Mat P, Mat Y, Mat Tw, double* ws, size_t ws_doubles, cudaStream_t st) {
+  static Comm* self = [] {
+    Comm* c[1];
+    new_local_group(1, c);
+    return c[0];
+  }();
+  const int m = P.rows, n = P.cols;
+  const int cap = panel_rows_max();
+  const size_t ts_n = tsqr_ws_doubles(m, n, 1, cap);
+  Arena ar{(char*)ws, ws_doubles * sizeof(double), 0};
+  double* ts = ar.take(ts_n);
+  const long ldn = round_up(n, 4);
+  double* Rn = ar.take((size_t)ldn * n);
+  double* rc = ar.take(reconstruct_ws_doubles(n));
+  if (!rc) return UTV_ERR_WORKSPACE;
+  UTV_CHECK(tsqr(self, P, Y, Mat{Rn, ldn, n, n}, cap, ts, ts_n, st));  // Q -> Y, P destroyed
+  UTV_CHECK(householder_reconstruct(self, Y, Tw, Mat{Rn, ldn, n, n}, rc,
+                                    reconstruct_ws_doubles(n), st));
+  UTV_CHECK(set_zero(P.p, P.ld, m, n, st));
+  return copy_mat(Rn, ldn, P.p, P.ld, n, n, st);
+}
+
 int geqrf(Mat P, Mat Y, Mat Tw, bool want_t, double* ws, size_t ws_doubles, cudaStream_t st) {
   if (P.rows < P.cols) return -1;
-  if (P.rows > panel_rows_max()) {
-    fprintf(stderr, "libutvb200: geqrf with %d rows exceeds the panel QR limit (%d)\n", P.rows,
-            panel_rows_max());
-    return -1;
-  }
+  if (P.rows > panel_rows_max()) return geqrf_tall(P, Y, Tw, ws, ws_doubles, st);
   Arena ar{(char*)ws, ws_doubles * sizeof(double), 0};
   double* fro2 = ar.take(8);
   double* red = ar.take(sumsq_scratch_doubles());

@@ -79,6 +79,10 @@ int copy_mat(const double* src, long lds, double* dst, long ldd, int rows, int c
 // LAPACK dlaset: uplo 0 all / 1 upper / 2 lower off-diagonal <- alpha, diagonal <- beta.
 int laset(int uplo, int rows, int cols, double alpha, double beta, double* A, long lda,
           cudaStream_t st);
+int laset_f32(int uplo, int rows, int cols, float alpha, float beta, float* A, long lda,
+              cudaStream_t st);
+// *flag (device int) <- 1 if any entry is NaN/Inf, else 0.
+int nonfinite(const double* A, long lda, int rows, int cols, int* flag, cudaStream_t st);
 // A <- alpha diag(d) A (side 0) or alpha A diag(d) (side 1).
 int diag_scale(int side, int rows, int cols, const double* d, double alpha, double* A, long lda,
                cudaStream_t st);
@@ -161,5 +165,32 @@ size_t lu_ws_doubles();
 size_t gesvj_ws_doubles(int n);
 int gesvj(Mat A, double* sigma, Mat U, Mat V, double* ws, size_t ws_doubles, int* status_dev,
           cudaStream_t st);
+
+// ---- communicators (comm.cu): collectives on FP64 device buffers, caller's stream ----
+struct Comm {
+  int rank = 0, size = 1;
+  virtual ~Comm() {}
+  virtual int allreduce_sum(double* buf, size_t count, cudaStream_t st) = 0;
+  // recv = [send of rank 0 | send of rank 1 | ...], count doubles each
+  virtual int allgather(const double* send, double* recv, size_t count, cudaStream_t st) = 0;
+  virtual int broadcast(double* buf, size_t count, int root, cudaStream_t st) = 0;
+};
+// P in-process ranks (threads); out[0..P-1] are owned by the caller (delete each).
+Comm* new_local_group(int nranks, Comm** out);
+
+// ---- TSQR + Householder reconstruction (tsqr.cu) ----
+// Thin QR of the row-sharded X (this rank: X.rows x n, X.rows >= n; X is
+// destroyed) into the explicit Q (this rank's rows) and the replicated R
+// (n x n, zeros below the diagonal).  Local row chunks of <= cap rows.
+size_t tsqr_ws_doubles(int m, int n, int nranks, int cap);
+int tsqr(Comm* comm, Mat X, Mat Q, Mat R, int cap, double* ws, size_t ws_doubles, cudaStream_t st);
+// Householder form (hqr_full semantics, qr.py:71-100) of a sharded explicit
+// thin Q: Q <- Y (this rank's rows), Tw <- the dense forward triangle,
+// R <- S R (replicated).  Rank 0 must own >= n rows.
+size_t reconstruct_ws_doubles(int n);
+int householder_reconstruct(Comm* comm, Mat Q, Mat Tw, Mat R, double* ws, size_t ws_doubles,
+                            cudaStream_t st);
+// Row-chunk cap of the single-launch panel QR (panel.cu) in use by geqrf.
+int tsqr_default_cap();
 
 }  // namespace utv

@@ -47,9 +47,14 @@ def check_matrix(a, name="matrix", finite=True):
 
 
 def raise_if_nonfinite(d, name="matrix"):
-    """The finite half of check_matrix, on a device copy (DMat)."""
+    """The finite half of check_matrix, on a device copy (DMat): one
+    libutvb200 scan (utv_dnonfinite) and a 4-byte read back."""
     import torch
-    if not bool(torch.isfinite(d.tensor()).all()):
+    from ._lib import check, load, stream_ptr
+    flag = torch.empty(1, dtype=torch.int32, device="cuda")
+    check(load().utv_dnonfinite(d.rows, d.cols, d.ptr, d.ld, flag.data_ptr(), stream_ptr()),
+          "utv_dnonfinite")
+    if int(flag.item()):
         raise ValueError(f"{name} contains NaN or Inf entries")
 
 

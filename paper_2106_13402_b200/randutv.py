@@ -20,6 +20,7 @@ from . import device as dv
 from ._lib import deye, dfrom_numpy
 from .errors import ConsistencyError, ConvergenceError, DimensionError
 from .matrix import raise_if_nonfinite, check_matrix, frobenius_norm
+from .svd import JACOBI_MAX_N
 
 
 @dataclass
@@ -90,6 +91,10 @@ def _validate(a, b, q, p, finite=True):
         raise ValueError(f"power iteration count must be >= 0, got {q}")
     if p < 0:
         raise ValueError(f"oversampling must be >= 0, got {p}")
+    # the b x b (and final <= (b+p)-wide) SVDs run in the Jacobi kernel (K6);
+    # checked before any draw so the caller's rng is untouched on failure
+    if min(int(b) + int(p), n) > JACOBI_MAX_N:
+        raise ValueError(f"b + p must be <= {JACOBI_MAX_N} on the B200 path, got {int(b) + int(p)}")
     return a
 
 
@@ -113,11 +118,9 @@ def randutv_basic_device(t_dev, b, q, g_dev, record_trailing=False):
 
 def _eye32(n):
     import torch
-    from ._lib import dempty
+    from ._lib import check, dempty, load, stream_ptr
     m = dempty(n, n, dtype=torch.float32)
-    m.t.zero_()
-    idx = torch.arange(n, device="cuda")
-    m.t[idx, idx] = 1.0
+    check(load().utv_slaset(b"A", n, n, 0.0, 1.0, m.ptr, m.ld, stream_ptr()), "utv_slaset")
     return m
 
 
@@ -202,8 +205,6 @@ def _randutv_stepwise(a, b, q, p, rng, boosted, tol_fro=None, max_rank=None,
     b, q, p = int(b), int(q), int(p)
     lib = _lib.load()
     pe = p if boosted else 0
-    if b + pe > 1024:
-        raise ValueError(f"b + p must be <= 1024 on the B200 path, got {b + pe}")
     t_dev = dfrom_numpy(a)
     U, V = deye(m), deye(n)
     steps_max = -(-n // b)

@@ -22,11 +22,19 @@ Only Vhat's column space matters for the next hqr_full (Householder vectors
 are invariant under column-sign flips of the input), so the
 inner thin QR needs no reconstruction.
 
-The algorithm is written once against two small interfaces: `Comm`
-(allreduce / allgather / broadcast) and an `ops` object (the device
-building blocks of libutvb200).  `TorchComm` runs it over torch.distributed
-(NCCL on GPUs); `ThreadComm` emulates P ranks as threads of one process
-sharing one GPU (used to validate the multi-rank logic on a single B200).
+PRODUCT PATH: `power_urv_sharded_native` — ONE C-ABI call per rank
+(utv_powerurv_sharded_f64, csrc/tsqr.cu) with the collectives inside
+libutvb200 on the caller's stream (`NativeComm`: NCCL bootstrapped through
+torch.distributed, or an in-process local group of P threads for
+single-GPU emulation).
+
+`power_urv_sharded` below is the same SPMD schedule written in Python
+against two small interfaces — `Comm` (allreduce / allgather / broadcast)
+and an `ops` object — the host-side mirror of tsqr.cu.  It lets the
+multi-rank logic run on CPU under torch.distributed/gloo with the numpy
+test backend (tests/numpy_ops.py) and on one B200 with `ThreadComm`
+(P ranks as threads), so the schedule is validated where no 8-GPU box is
+available.
 """
 
 from __future__ import annotations
@@ -306,12 +314,16 @@ def q_times_top(y, t, top, out, ops):
 
 def householder_from_q(q, r_in, comm, ops):
     """Compact-WY factor (Y_i rows, Twy) and R of hqr_full for the sharded
-    explicit thin Q (LAPACK dorhr_col; lu.cu).  Rank 0 must own >= n rows."""
+    explicit thin Q (LAPACK dorhr_col; lu.cu).  Rank 0 must own >= n rows.
+
+    Only the top n x n block is factored (on rank 0): Q_0[:n] - S = L11 U'.
+    It is broadcast with S, and every rank then forms its own rows of
+    Y = Q U'^{-1} by a triangular solve (the rows below the top block are
+    unshifted, so L21 = Q21 U'^{-1}); rank 0's top rows are L11."""
     m, n = ops.shape(q)
     if comm.rank == 0:
-        w = ops.copy(q)
-        s = ops.getrf_signed(w)                  # w = L \\ U' (top n x n), L below
-        top = ops.copy(ops.sub(w, 0, 0, n, n))
+        top = ops.copy(ops.sub(q, 0, 0, n, n))
+        s = ops.getrf_signed(top)                # top = L11 \ U'
     else:
         top = ops.empty(n, n)
         s = None
@@ -321,11 +333,14 @@ def householder_from_q(q, r_in, comm, ops):
         comm.broadcast_(ttop, 0)
         top = ops.from_comm(ttop, n, n)
         s = comm.broadcast_(s if s is not None else _vec_like(ttop, n), 0)
+    y = q
     if comm.rank == 0:
-        y = w
-        ops.laset("U", 0.0, 1.0, ops.sub(y, 0, 0, n, n))   # unit lower L11 on top
+        y1 = ops.sub(y, 0, 0, n, n)
+        ops.lacpy(top, y1)
+        ops.laset("U", 0.0, 1.0, y1)                       # unit lower L11 on top
+        if m > n:
+            ops.trsm_right("U", "N", "N", top, ops.sub(y, n, 0, m - n, n))
     else:
-        y = ops.copy(q)
         ops.trsm_right("U", "N", "N", top, y)              # Y_i = Q_i U'^{-1}
     # Twy = -U' S L11^{-T}, redundantly on every rank
     tw = ops.copy(top)
@@ -379,3 +394,101 @@ def power_urv_sharded(a_loc, g, q, comm=None, ops=None, chunk_rows=None):
     del ahat
     uy, ut, r, _ = householder_from_q(qh, r_in, comm, ops)
     return {"Uy": uy, "Ut": ut, "R": r, "Vy": vy, "Vt": vt}
+
+
+# ---------------------------------------------------------------------------
+# product path: the whole SPMD schedule inside libutvb200 (csrc/tsqr.cu)
+# ---------------------------------------------------------------------------
+
+class NativeComm:
+    """A libutvb200 communicator (utv_comm_t, csrc/comm.cu)."""
+
+    def __init__(self, handle):
+        from ._lib import load
+        self._lib = load()
+        self.handle = handle
+        self.rank = self._lib.utv_comm_rank(handle)
+        self.size = self._lib.utv_comm_size(handle)
+
+    @classmethod
+    def nccl(cls, group=None):
+        """NCCL communicator over the ranks of a torch.distributed group (one
+        process per GPU, current device bound); torch.distributed only ships
+        the 128-byte unique id from rank 0."""
+        import ctypes
+
+        import torch.distributed as dist
+        from ._lib import check, load
+        lib = load()
+        rank, size = dist.get_rank(group), dist.get_world_size(group)
+        buf = ctypes.create_string_buffer(128)
+        if rank == 0:
+            check(lib.utv_comm_nccl_unique_id(buf), "utv_comm_nccl_unique_id")
+        obj = [buf.raw if rank == 0 else None]
+        src = 0 if group is None else dist.get_global_rank(group, 0)
+        dist.broadcast_object_list(obj, src=src, group=group)
+        uid = ctypes.create_string_buffer(obj[0], 128)
+        h = ctypes.c_void_p()
+        check(lib.utv_comm_init_nccl(uid, size, rank, ctypes.byref(h)), "utv_comm_init_nccl")
+        return cls(h.value)
+
+    @classmethod
+    def nccl_single(cls):
+        """A 1-rank NCCL communicator (no torch.distributed needed)."""
+        import ctypes
+
+        from ._lib import check, load
+        lib = load()
+        uid = ctypes.create_string_buffer(128)
+        check(lib.utv_comm_nccl_unique_id(uid), "utv_comm_nccl_unique_id")
+        h = ctypes.c_void_p()
+        check(lib.utv_comm_init_nccl(uid, 1, 0, ctypes.byref(h)), "utv_comm_init_nccl")
+        return cls(h.value)
+
+    @classmethod
+    def local_group(cls, size):
+        """`size` in-process ranks (drive each from its own thread + stream)."""
+        import ctypes
+
+        from ._lib import check, load
+        hs = (ctypes.c_void_p * size)()
+        check(load().utv_comm_init_local(size, hs), "utv_comm_init_local")
+        return [cls(hs[r]) for r in range(size)]
+
+    def close(self):
+        if self.handle:
+            self._lib.utv_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001  (interpreter shutdown)
+            pass
+
+
+def power_urv_sharded_native(a_loc, g, q, comm, chunk_rows=None):
+    """Row-sharded powerURV (power_urv_from_sample, powerurv.py:41-72): one
+    utv_powerurv_sharded_f64 call on this rank.  a_loc: this rank's rows of A
+    (DMat, m_i x n, m_i >= n); g: the replicated n x n G (DMat); comm: a
+    NativeComm.  Returns dict(Uy = this rank's rows of Uq.Y, Ut, R (n x n),
+    Vy, Vt) as DMats.  Every rank must call it (collective); it runs on
+    torch's current stream (the workspace is released to the caching
+    allocator in that stream's order)."""
+    from ._lib import check, dempty, load, stream_ptr, workspace
+    lib = load()
+    m, n = a_loc.rows, a_loc.cols
+    if q < 0:
+        raise ValueError(f"power iteration count must be >= 0, got {q}")
+    cr = int(chunk_rows or 0)
+    out = {"Uy": dempty(m, n), "Ut": dempty(n, n), "R": dempty(n, n), "Vy": dempty(n, n),
+           "Vt": dempty(n, n)}
+    lw = lib.utv_powerurv_sharded_bufsize(m, n, comm.size, cr)
+    ws = workspace(lw)
+    st = stream_ptr()
+    check(lib.utv_powerurv_sharded_f64(
+        comm.handle, m, n, int(q), a_loc.ptr, a_loc.ld, g.ptr, g.ld,
+        out["Uy"].ptr, out["Uy"].ld, out["Ut"].ptr, out["Ut"].ld, out["R"].ptr, out["R"].ld,
+        out["Vy"].ptr, out["Vy"].ld, out["Vt"].ptr, out["Vt"].ld, cr, ws.data_ptr(), lw, st),
+        "utv_powerurv_sharded_f64")
+    return out

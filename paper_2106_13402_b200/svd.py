@@ -14,11 +14,15 @@ import numpy as np
 
 from ._lib import serialized as _serialized
 from . import device as dv
-from ._lib import dfrom_numpy
-from .errors import ConvergenceError
+from ._lib import dempty, dfrom_numpy
+from .errors import ConvergenceError, DimensionError
 from .matrix import check_matrix
 
-MAX_N = 400
+#: Largest n the one-sided Jacobi kernel (utv_dgesvj, csrc/jacobi.cu) takes:
+#: one cooperative grid holds the n x n block and its V in L2 / shared memory
+#: and the finish kernel keeps a column per thread (1024 threads).
+JACOBI_MAX_N = 1024
+MAX_N = JACOBI_MAX_N
 
 
 @dataclass(frozen=True)
@@ -62,7 +66,8 @@ def svd_dense(a, mode="full"):
         _sign_fix(u[:, :r], v[:, :r])
         return SvdTriple(U=u, sigma=t.sigma, V=v, thin=(mode == "thin"))
     if n > MAX_N:
-        raise ValueError(f"svd_dense on the B200 path supports min(m, n) <= {MAX_N}")
+        raise ValueError(f"svd_dense on the B200 path supports min(m, n) <= {MAX_N} "
+                         "(the Jacobi kernel's limit)")
     if m == n:
         sig, U, V = _jacobi(dfrom_numpy(a))
         return SvdTriple(U=np.asfortranarray(U.to_numpy()), sigma=sig.cpu().numpy()[:n].copy(),
@@ -83,3 +88,27 @@ def svd_dense(a, mode="full"):
         u = dc
     return SvdTriple(U=np.asfortranarray(u.to_numpy()), sigma=sig.cpu().numpy()[:n].copy(),
                      V=np.asfortranarray(V.to_numpy()), thin=(mode == "thin"))
+
+
+@_serialized
+def svd_tall_thin_left(y):
+    """Left singular vectors of a tall thin y (n x w, n >= w) completed to an
+    orthogonal n x n W = Q blockdiag(Uhat, I) (svd.py:61-82): one device
+    Householder QR of y, the w x w Jacobi SVD of R[:w, :], one compact-WY
+    apply of Q to the block-diagonal completion.  w <= JACOBI_MAX_N."""
+    y = check_matrix(y)
+    n, w = y.shape
+    if n < w:
+        raise DimensionError(f"svd_tall_thin_left needs rows >= cols, got {y.shape}")
+    if w > JACOBI_MAX_N:
+        raise ValueError(f"svd_tall_thin_left on the B200 path supports cols <= {JACOBI_MAX_N}")
+    d = dfrom_numpy(y)
+    Y, T = dv.geqrf(d)                       # d <- R (zeros below the diagonal)
+    r = dempty(w, w)
+    dv.lacpy(d.sub(0, 0, w, w), r)
+    _, uhat, _ = _jacobi(r)
+    c = dempty(n, n)
+    dv.laset("A", 0.0, 1.0, c)
+    dv.lacpy(uhat, c.sub(0, 0, w, w))
+    dv.larfb("L", False, Y, T, c)
+    return np.asfortranarray(c.to_numpy())

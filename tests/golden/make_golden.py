@@ -194,8 +194,33 @@ def hqrcp():
         print("wrote", name)
 
 
+def rsvd():
+    """Reference rsvd / projector_gap (rsvd.py:31-78) for SPEC acceptance 2:
+    shared-G powerURV vs RSVD on a Gaussian 60x40 for every (ell, q)."""
+    sys.dont_write_bytecode = True
+    sys.path.insert(0, REF)
+    import utvkit as uk  # noqa: E402
+    rng = uk.RngStream(81)
+    a = uk.gen_gaussian(60, rng)[:, :40].copy(order="F")
+    g = uk.gaussian(40, 40, rng)
+    out = dict(A=a, G=g, ells=np.array([1, 5, 10, 20, 40]), qs=np.array([0, 1, 2]))
+    for q in (0, 1, 2):
+        urv = uk.power_urv_from_sample(a, q, g)
+        for ell in (1, 5, 10, 20, 40):
+            rs = uk.rsvd(a, g, ell, q)
+            out[f"U_rsvd_q{q}_l{ell}"] = rs.U_rsvd
+            out[f"sigma_q{q}_l{ell}"] = rs.sigma
+            out[f"gap_q{q}_l{ell}"] = uk.projector_gap(uk.materialize_q(urv.Uq, ell), rs.U_rsvd, a)
+    np.savez_compressed(os.path.join(OUT, "rsvd_gauss60x40.npz"),
+                        call="rsvd(A,G,ell,q); projector_gap(materialize_q(power_urv_from_sample(A,q,G).Uq,ell),"
+                             " U_rsvd, A)", **out)
+    print("wrote rsvd_gauss60x40.npz")
+
+
 if __name__ == "__main__":
-    if len(sys.argv) > 1 and sys.argv[1] == "hqrcp":
+    if len(sys.argv) > 1 and sys.argv[1] == "rsvd":
+        rsvd()
+    elif len(sys.argv) > 1 and sys.argv[1] == "hqrcp":
         hqrcp()
     elif len(sys.argv) > 1 and sys.argv[1] == "boosted":
         boosted()

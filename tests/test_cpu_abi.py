@@ -101,7 +101,66 @@ def test_cli_usage_and_exit_codes(tmp_path):
     assert cli.main(["bogus"]) == 1
     a = np.arange(12.0).reshape(4, 3) + 0.5
     p = tmp_path / "a.mtx"
-    cli.write_matrix(a, str(p))
-    assert np.array_equal(cli.read_matrix(str(p)), a)    # %.17g round-trips bitwise
-    # comparators are not on the B200 path: ValueError -> exit 1
-    assert cli.main(["factor", "--algo", "svd", "--in", str(p), "--out-prefix", str(tmp_path / "f")]) == 1
+    cli.save_text(a, str(p))
+    assert np.array_equal(cli.load_text(str(p)), a)    # %.17g round-trips bitwise
+    assert cli.main(["factor", "--algo", "nope", "--in", str(p), "--out-prefix", "x"]) == 1
+    # missing input file: OSError -> exit 1 (cli.py:248-253)
+    assert cli.main(["factor", "--algo", "randutv", "--in", str(tmp_path / "missing.mtx"),
+                     "--out-prefix", str(tmp_path / "f")]) == 1
+    assert cli.main(["--backend", "cuda", "time"]) == 1
+
+
+def test_cli_plugs_into_the_reference_harness(tmp_path, monkeypatch):
+    """Plug-in mode: with utvkit importable, the reference's own harness runs;
+    --backend b200 serves its factorisation names from this package for the
+    duration of the call, --backend reference leaves it untouched."""
+    import sys
+
+    ref = "/root/reference/pkg/src"
+    if not os.path.isdir(ref):
+        pytest.skip("reference package not present (GPU box)")
+    monkeypatch.setattr(sys, "path", [ref] + sys.path)
+    monkeypatch.setattr(sys, "dont_write_bytecode", True)
+    import paper_2106_13402_b200 as pk
+    from paper_2106_13402_b200 import cli
+    refcli = cli.reference_cli()
+    assert refcli is not None
+    orig = refcli.power_urv
+    with cli.b200_backend(refcli):
+        assert refcli.power_urv is pk.power_urv
+        assert refcli.randutv_basic is pk.randutv_basic
+        assert refcli.hqrcp is pk.hqrcp
+    assert refcli.power_urv is orig
+    out = tmp_path / "g.mtx"
+    assert cli.main(["--backend", "reference", "gen", "--kind", "gaussian", "--n", "6",
+                     "--seed", "3", "--out", str(out)]) == 0
+    import utvkit
+    a = utvkit.read_matrix(str(out))
+    assert np.array_equal(a, utvkit.gen_gaussian(6, utvkit.RngStream(3)))
+    assert np.array_equal(cli.load_text(str(out)), a)
+    assert cli.main(["--backend", "reference", "time"]) == 1        # the reference's usage exit
+
+
+def test_comm_and_sharded_validation_without_device():
+    """utv_comm_* / utv_powerurv_sharded_f64 argument checks (no device): the
+    local-group communicator is host-only state; null handles are rejected."""
+    import ctypes
+
+    from paper_2106_13402_b200 import _lib
+    lib = _lib.load()
+    assert lib.utv_comm_init_local(0, None) == -1
+    hs = (ctypes.c_void_p * 3)()
+    assert lib.utv_comm_init_local(3, hs) == 0
+    assert [lib.utv_comm_rank(hs[r]) for r in range(3)] == [0, 1, 2]
+    assert all(lib.utv_comm_size(hs[r]) == 3 for r in range(3))
+    assert lib.utv_comm_broadcast_f64(hs[0], None, 0, 5, None) == -4
+    for r in range(3):
+        assert lib.utv_comm_destroy(hs[r]) == 0
+    assert lib.utv_comm_rank(None) == -1
+    assert lib.utv_comm_allreduce_sum_f64(None, None, 1, None) == -1
+    assert lib.utv_comm_init_nccl(None, 1, 0, None) == -1
+    assert lib.utv_powerurv_sharded_f64(None, 10, 4, 1, 0, 10, 0, 4, 0, 10, 0, 4, 0, 4, 0, 4, 0, 4,
+                                        0, 0, 0, None) == -1
+    assert lib.utv_powerurv_sharded_bufsize(524288, 4096, 1, 0) > 2 * 524288 * 4096 * 8
+    assert lib.utv_dnonfinite(-1, 2, 0, 2, 0, None) == -1
+    assert lib.utv_slaset(b"X", 2, 2, 0.0, 1.0, 0, 2, None) == -1

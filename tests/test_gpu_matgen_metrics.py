@@ -55,10 +55,14 @@ def test_cli_time_and_factor(tmp_path, capsys):
     assert cli.main(["gen", "--kind", "fast", "--n", "120", "--out", str(tmp_path / "a.mtx")]) == 0
     assert cli.main(["factor", "--algo", "randutv", "--b", "32", "--q", "1", "--in", str(tmp_path / "a.mtx"),
                      "--out-prefix", str(tmp_path / "f")]) == 0
-    a = cli.read_matrix(str(tmp_path / "a.mtx"))
-    u, t, v = (cli.read_matrix(str(tmp_path / f"f.{x}.mtx")) for x in "UTV")
+    a = cli.load_text(str(tmp_path / "a.mtx"))
+    u, t, v = (cli.load_text(str(tmp_path / f"f.{x}.mtx")) for x in "UTV")
     assert np.linalg.norm(a - u @ t @ v.T) / np.linalg.norm(a) < 1e-13
-    assert cli.main(["curve", "--factors", str(tmp_path / "f"), "--csv", str(tmp_path / "e.csv")]) == 0
+    assert cli.main(["errors", "--in", str(tmp_path / "a.mtx"), "--factors", str(tmp_path / "f"),
+                     "--norm", "fro", "--csv", str(tmp_path / "e.csv")]) == 0
+    rows = (tmp_path / "e.csv").read_text().splitlines()
+    assert rows[0] == "k,e_k,e_opt,rel" and len(rows) == 120
+    assert cli.main(["check-rsvd", "--n", "64", "--ell", "8", "--q", "1"]) == 0
     assert cli.main(["time", "--algo", "powerurv", "--n", "200", "--q", "1", "--reps", "2",
                      "--csv", str(tmp_path / "t.csv")]) == 0
     out = capsys.readouterr().out
@@ -71,7 +75,34 @@ def test_cli_cpqr_factor(tmp_path):
     assert cli.main(["gen", "--kind", "kahan", "--n", "60", "--out", str(tmp_path / "k.mtx")]) == 0
     assert cli.main(["factor", "--algo", "cpqr", "--in", str(tmp_path / "k.mtx"),
                      "--out-prefix", str(tmp_path / "c")]) == 0
-    a = cli.read_matrix(str(tmp_path / "k.mtx"))
-    u, t, v = (cli.read_matrix(str(tmp_path / f"c.{x}.mtx")) for x in "UTV")
+    a = cli.load_text(str(tmp_path / "k.mtx"))
+    u, t, v = (cli.load_text(str(tmp_path / f"c.{x}.mtx")) for x in "UTV")
     assert np.linalg.norm(a - u @ t @ v.T) / np.linalg.norm(a) < 1e-13
     assert np.abs(np.tril(t, -1)).max() == 0.0
+
+
+def test_cli_b200_backend_inside_the_reference_harness(tmp_path):
+    """Plug-in mode on the GPU box: the reference harness (the unmodified copy
+    oracle/_ref, test infrastructure) drives this package's randUTV through
+    `--backend b200`; the factors it writes reconstruct A."""
+    import sys
+
+    from oracle import build_ref
+    if not build_ref.available():
+        pytest.skip("oracle/_ref not built")
+    build_ref.load()                      # puts the verified copy on sys.path as `utvkit`
+    from paper_2106_13402_b200 import cli
+    assert cli.reference_cli() is not None
+    a_path = tmp_path / "a.mtx"
+    assert cli.main(["gen", "--kind", "gaussian", "--n", "96", "--out", str(a_path)]) == 0
+    assert cli.main(["factor", "--algo", "randutv", "--b", "32", "--q", "1", "--in", str(a_path),
+                     "--out-prefix", str(tmp_path / "f")]) == 0
+    a = cli.load_text(str(a_path))
+    u, t, v = (cli.load_text(str(tmp_path / f"f.{x}.mtx")) for x in "UTV")
+    assert np.linalg.norm(a - u @ t @ v.T) / np.linalg.norm(a) < 1e-13
+    assert cli.main(["errors", "--in", str(a_path), "--factors", str(tmp_path / "f"),
+                     "--norm", "fro", "--csv", str(tmp_path / "e.csv")]) == 0
+    for mod in [m for m in sys.modules if m == "utvkit" or m.startswith("utvkit.")]:
+        sys.modules.pop(mod)
+    if build_ref.DST_ROOT in sys.path:
+        sys.path.remove(build_ref.DST_ROOT)

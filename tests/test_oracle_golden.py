@@ -111,3 +111,18 @@ def test_oracle_hqrcp_matches_reference(golden, name):
     assert np.abs(r - g["R"]).max() <= 1e-13 * scale
     assert np.abs(y - g["Y"]).max() <= 1e-12
     assert np.abs(t - g["Twy"]).max() <= 1e-12
+
+
+def test_oracle_rsvd_matches_reference(golden):
+    """The oracle's rsvd / projector_gap restatement against the reference's
+    own outputs (tests/golden/make_golden.py rsvd)."""
+    z = golden("rsvd_gauss60x40")
+    a, g = z["A"], z["G"]
+    for q in (0, 1, 2):
+        urv = orc.power_urv(a, q, g)
+        for ell in (1, 5, 10, 20, 40):
+            u, s, _ = orc.rsvd(a, g, ell, q)
+            assert np.abs(s - z[f"sigma_q{q}_l{ell}"]).max() < 1e-12 * s[0]
+            assert np.abs(np.abs(u) - np.abs(z[f"U_rsvd_q{q}_l{ell}"])).max() < 1e-10
+            gap = orc.projector_gap(orc.wy_materialize(urv["Uy"], urv["Ut"], ell), u, a)
+            assert gap <= 1e-10 and abs(gap - float(z[f"gap_q{q}_l{ell}"])) < 1e-12
