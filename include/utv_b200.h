@@ -17,8 +17,19 @@
  *    point synchronises the host; results are ready when the stream is.
  *  - Return value: 0 ok; -i = argument i is invalid (LAPACK `info` style);
  *    -1000 CUDA error; -1001 workspace too small; -1002 alignment;
+ *    -1003 wrong device (see the process model); -1004 communicator error;
  *    > 0 numerical failure reported through a device status word.
  *  - Deterministic: identical inputs give bitwise identical outputs.
+ *  - Process model: one device per process.  The library binds to the
+ *    first device it is used on (side streams, events, tile-scheduler slots
+ *    and split-K turn counters live there); the drivers and the sharded
+ *    entry return -1003 when called with another current device.  Calls
+ *    from several host threads are safe on distinct caller streams; the
+ *    side-stream drivers (utv_randutv_basic_f64 / _steps_f64 / _step_f64 /
+ *    _f32, utv_powerurv_f64*) enqueue under a process-wide lock, and the
+ *    step ranges of ONE factorisation (utv_randutv_basic_steps_f64,
+ *    utv_randutv_step_f64) must not interleave with another randUTV call.
+ *    (The Python package serialises its public calls.)
  */
 #ifndef UTV_B200_H
 #define UTV_B200_H

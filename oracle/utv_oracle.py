@@ -479,6 +479,11 @@ def decay_matrix(n, beta, seed, m=None):
     gen = gaussian_stream(seed)
     m = n if m is None else m
     d = beta ** (np.arange(n) / max(n - 1, 1))
-    q1 = random_orthogonal_fast(m, gen)[:, :n]
+    if m == n:
+        q1 = random_orthogonal_fast(m, gen)
+    else:                                   # thin factor: never form an m x m matrix
+        g = gen.standard_normal((m, n))
+        qm, rm = np.linalg.qr(g)
+        q1 = qm * np.sign(np.diag(rm))[None, :]
     q2 = random_orthogonal_fast(n, gen)
     return np.asfortranarray(q1 @ (d[:, None] * q2.T)), d

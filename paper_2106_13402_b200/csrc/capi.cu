@@ -35,6 +35,12 @@ static inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
 static inline size_t B(size_t doubles) { return doubles * sizeof(double) + 4096; }
 static inline bool ld_ok(long ld, int rows) { return ld >= (rows > 1 ? rows : 1) && (ld & 1) == 0; }
 
+// Drivers on the shared side streams/events: bound-device check, then the
+// enqueue runs under the process-wide driver lock (streams.cu).
+#define UTV_DRIVER_GUARD()                                 \
+  UTV_CHECK(check_device());                               \
+  std::lock_guard<std::mutex> driver_lock_(driver_mutex())
+
 extern "C" {
 
 int utv_version(void) { return 100; }
@@ -142,6 +148,7 @@ int utv_randutv_basic_steps_f64(int i0, int i1, int m, int n, int b, int q, doub
   if (!ld_ok(ldt, m)) return -8;
   if (!ld_ok(ldu, m)) return -10;
   if (!ld_ok(ldv, n)) return -12;
+  UTV_DRIVER_GUARD();
   return randutv_basic_range(i0, i1, m, n, b, q, Mat{T, ldt, m, n}, Mat{U, ldu, m, m},
                              Mat{V, ldv, n, n}, G, ldg, errsq, trail2, svd_status, (double*)work,
                              lwork / sizeof(double), S(stream));
@@ -162,6 +169,7 @@ int utv_randutv_step_f64(int i, int m, int n, int b, int p, int q, int boosted, 
   if (!ld_ok(ldu, m)) return -11;
   if (!ld_ok(ldv, n)) return -13;
   if (!carried || !is_final) return -19;
+  UTV_DRIVER_GUARD();
   return randutv_step(i, m, n, b, boosted ? p : 0, q, boosted != 0, Mat{T, ldt, m, n},
                       Mat{U, ldu, m, m}, Mat{V, ldv, n, n}, G, ldg, errsq, trail2, svd_status,
                       (double*)work, lwork / sizeof(double), carried, is_final, S(stream));
@@ -178,6 +186,7 @@ int utv_randutv_basic_f32(int m, int n, int b, int q, float* T, long ldt, float*
   if (ldt < m) return -6;
   if (ldu < m) return -8;
   if (ldv < n) return -10;
+  UTV_DRIVER_GUARD();
   return randutv_basic_f32(m, n, b, q, T, ldt, U, ldu, V, ldv, G, ldg, errsq, trail2, svd_status,
                            work, lwork, S(stream));
 }
@@ -364,6 +373,7 @@ int utv_randutv_basic_f64(int m, int n, int b, int q, double* T, long ldt, doubl
   if (!ld_ok(ldu, m)) return -8;
   if (!ld_ok(ldv, n)) return -10;
   if (n > b && !ld_ok(ldg, b)) return -12;
+  UTV_DRIVER_GUARD();
   return randutv_basic(m, n, b, q, Mat{T, ldt, m, n}, Mat{U, ldu, m, m}, Mat{V, ldv, n, n}, G, ldg,
                        errsq, trail2, svd_status, (double*)work, lwork / sizeof(double),
                        S(stream));
@@ -393,6 +403,7 @@ int utv_powerurv_f64_ev(int m, int n, int q, const double* A, long lda, const do
   if (!ld_ok(ldr, m)) return -13;
   if (!ld_ok(ldvy, n)) return -15;
   if (!ld_ok(ldvt, n)) return -17;
+  UTV_DRIVER_GUARD();
   return powerurv(m, n, q, Mat{(double*)A, lda, m, n}, Mat{(double*)G, ldg, n, n},
                   Mat{Uy, lduy, m, n}, Mat{Ut, ldut, n, n}, Mat{R, ldr, m, n}, Mat{Vy, ldvy, n, n},
                   Mat{Vt, ldvt, n, n}, (double*)work, lwork / sizeof(double), S(stream),
@@ -414,6 +425,7 @@ int utv_powerurv_f64_yhat(int m, int n, int q, const double* A, long lda, const 
   if (!ld_ok(ldr, m)) return -13;
   if (!ld_ok(ldvy, n)) return -15;
   if (!ld_ok(ldvt, n)) return -17;
+  UTV_DRIVER_GUARD();
   return powerurv(m, n, q, Mat{(double*)A, lda, m, n}, Mat{nullptr, n, n, n},
                   Mat{Uy, lduy, m, n}, Mat{Ut, ldut, n, n}, Mat{R, ldr, m, n}, Mat{Vy, ldvy, n, n},
                   Mat{Vt, ldvt, n, n}, (double*)work, lwork / sizeof(double), S(stream),
@@ -439,6 +451,7 @@ int utv_powerurv_sharded_f64(utv_comm_t comm, int m_local, int n, int q, const d
   else if (!ld_ok(ldvy, n)) bad = -16;
   else if (!ld_ok(ldvt, n)) bad = -18;
   if (bad) m_local = -1;  // forces the agreed failure path
+  UTV_CHECK(check_device());
   const int rc = powerurv_sharded((Comm*)comm, m_local, n, q, Mat{(double*)A, lda, m_local, n},
                                   Mat{(double*)G, ldg, n, n}, Mat{Uy, lduy, m_local, n},
                                   Mat{Ut, ldut, n, n}, Mat{R, ldr, n, n}, Mat{Vy, ldvy, n, n},

@@ -67,7 +67,21 @@ struct Args {
   double* ws;  // split-K partials [split][N][M] (ld = M)
   int* sched;  // dynamic tile scheduler [ticket, done] (self-resetting), or null = static
   int tri_a;   // A (N-major, M == K, unshifted) is upper triangular: skip k-blocks below the tile
+  // fused split-K: split z of an output tile adds its partial to the running
+  // sum of splits < z (tile-major ws, 128x128 per tile) after a per-tile
+  // semaphore says z's turn; the last split applies alpha/beta to C.  Same
+  // summation order as the separate reduce kernel -> the same bits.
+  int* flags;  // per-tile turn counters (self-resetting), null = separate reduce kernel
 };
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 // Physical double offset inside a 128B-swizzled tile whose 128-byte line is
 // `line` and whose logical element within that line is `idx` (0..15).
@@ -267,7 +281,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    if (HASC && ptile >= 0) load_c(ptile);
+    if (HASC && p.beta != 0.0 && ptile >= 0) load_c(ptile);
     for (int i = 0; i < STAGES - 1; ++i) produce_one();
   }
 
@@ -328,7 +342,53 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     // ---------------- epilogue ----------------
     const int m0 = tc.mc - (TA ? 0 : p.a_sh), n0 = tc.nc - (TB ? p.b_sh : 0);
-    if (HASC) mbar_wait(cfull, (uint32_t)(local & 1));
+    if (!HASC && p.flags) {
+      // fused split-K (no C tile prefetch: splits > 1 never has HASC)
+      const int per = p.tm * p.tn;
+      const int r = tile - tc.z * per;
+      const int zf = p.tri_a ? ((tc.mc / BK) * BK) / p.k_split : 0;   // first non-empty split
+      const int zl = p.tiles / per - 1;
+      const bool first = tc.z == zf, last = tc.z == zl;
+      double* wt = p.ws + (size_t)r * (BM * BN);
+      if (!first) {
+        if (threadIdx.x == 0) {
+          while (ld_acquire(p.flags + r) != tc.z - zf) __nanosleep(64);
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int ml = frag_row<TA>(wm, t, fr);
+        const int m = m0 + ml;
+        const bool mok = (m >= 0 && m < p.M);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int nl = frag_col<TB>(wn, u, 2 * fk + j);
+            double* wp = wt + ml + nl * BM;
+            double v = acc[t][u][j];
+            if (!first) v = __ldcg(wp) + v;                 // splits summed in split order
+            if (!last) {
+              __stcg(wp, v);
+            } else {
+              const int n = n0 + nl;
+              if (mok && n >= 0 && n < p.N) {
+                double* c = p.C + m + (long)n * p.ldc;
+                *c = (p.beta == 0.0) ? p.alpha * v : fma(p.beta, *c, p.alpha * v);
+              }
+            }
+          }
+      }
+      __syncthreads();  // every thread's partial stores issued
+      if (threadIdx.x == 0) {
+        __threadfence();
+        if (last) p.flags[r] = 0;                          // reset for the next launch
+        else st_release(p.flags + r, tc.z - zf + 1);
+      }
+      continue;
+    }
+    if (HASC && p.beta != 0.0) mbar_wait(cfull, (uint32_t)(local & 1));
     double* w = p.ws ? p.ws + (size_t)tc.z * p.N * p.M : nullptr;
     // beta != 0 with an unshifted C map: alpha*acc + beta*C is written back
     // over the prefetched C tile in smem and leaves by one TMA store, so the
@@ -353,7 +413,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           double v = p.alpha * acc[t][u][j];
           if (HASC) {
             double* cs = &sC[swz((ml >> 4) * BN + nl, ml & 15)];
-            v = fma(p.beta, *cs, v);
+            if (p.beta != 0.0) v = fma(p.beta, *cs, v);
             if (tstore) {
               *cs = v;
               continue;
@@ -376,7 +436,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           bulk_wait_read0();  // sC may be refilled once the store has read it
         }
         const int nxt = tq[(local + 1) & 7];  // published: the producer runs >= 1 k-block ahead
-        if (nxt >= 0) load_c(nxt);
+        if (nxt >= 0 && p.beta != 0.0) load_c(nxt);
       }
     }
   }
@@ -489,6 +549,21 @@ int* gemm_sched_slot(cudaStream_t st) {
   if (g_sched_n == 64) return nullptr;  // fall back to static scheduling
   g_sched_streams[g_sched_n] = st;
   return g_sched + 2 * (g_sched_n++);
+}
+
+// ---- fused split-K turn counters: FLAG_TILES per stream slot ----
+constexpr int FLAG_TILES = 4096;
+static int* g_flags = nullptr;
+
+static int* gemm_flag_slot(cudaStream_t st) {
+  int* sched = gemm_sched_slot(st);  // same slot index as the tile scheduler
+  if (!sched) return nullptr;
+  std::lock_guard<std::mutex> lk(g_sched_mu);
+  if (!g_flags) {
+    if (cudaMalloc((void**)&g_flags, sizeof(int) * 64 * FLAG_TILES) != cudaSuccess) return nullptr;
+    if (cudaMemset(g_flags, 0, sizeof(int) * 64 * FLAG_TILES) != cudaSuccess) return nullptr;
+  }
+  return g_flags + (size_t)((sched - g_sched) / 2) * FLAG_TILES;
 }
 
 // CTA budget of the next GEMM launches on this host thread (0 = all SMs):
@@ -660,7 +735,15 @@ int dgemm_ex(bool ta, bool tb, int M, int N, int K, double alpha, const double* 
 
   // beta != 0 without split-K: the C tile is TMA-prefetched; its map must
   // share the A tile's row parity (always true for even offsets).
-  bool hasc = (beta != 0.0) && splits == 1;
+  // beta == 0 may also take the smem-staged epilogue (accumulators -> smem ->
+  // one TMA store, no C prefetch): the warps start the next tile after the
+  // ~0.5 us smem write instead of ~2 us of direct global stores, at the
+  // price of the 3-stage ring.  Tuning knob UTV_GEMM_TSTORE0 (0 = off).
+  static const bool tstore0 = [] {
+    const char* e = getenv("UTV_GEMM_TSTORE0");
+    return e ? atoi(e) != 0 : false;
+  }();
+  bool hasc = (beta != 0.0 || tstore0) && splits == 1;
   CUtensorMap mC = mA;
   int c_sh = 0;
   if (hasc) {
@@ -689,6 +772,19 @@ int dgemm_ex(bool ta, bool tb, int M, int N, int K, double alpha, const double* 
   a.ws = use_ws ? ws : nullptr;
   a.sched = gemm_sched_slot(st);
   a.tri_a = tri ? 1 : 0;
+  // Fused split-K when the dynamic scheduler is on (tickets in split-major
+  // order: a split only ever waits for a lower ticket, already held by a
+  // running CTA -> no deadlock), the per-tile sums fit the workspace
+  // tile-major, and the serial chain of S epilogues stays short.
+  static const int fuse_max = [] {
+    const char* e = getenv("UTV_SPLITK_FUSE_MAX");  // tuning knob (0 = always the reduce kernel)
+    return e ? atoi(e) : 4;
+  }();
+  a.flags = nullptr;
+  if (splits > 1 && splits <= fuse_max && a.sched && tm * tn <= FLAG_TILES &&
+      (size_t)tm * tn * gemm::BM * gemm::BN <= ws_doubles)
+    a.flags = gemm_flag_slot(st);
+  const bool fused = a.flags != nullptr;
   double fl = 2.0 * M * N * K;
   if (tri) {
     fl = 0.0;
@@ -722,7 +818,7 @@ int dgemm_ex(bool ta, bool tb, int M, int N, int K, double alpha, const double* 
   }
   UTV_CUDA(cudaGetLastError());
   }
-  if (use_ws) {
+  if (use_ws && !fused) {
     const long total = (long)M * N;
     ProfScope ps(PROF_SPLITK, 0.0, 8.0 * (splits + (beta != 0.0 ? 2 : 1)) * total, st);
     const int gx = ceil_div(ceil_div(M, 2), 256);

@@ -39,7 +39,7 @@ static size_t plan_purv(int m, int n, PurvWs* w, double* base) {
   v.ldm = round_up(m, 4);
   v.ldn = round_up(n, 4);
   v.qr_n = geqrf_ws_doubles(m, n, true);
-  v.lfb_n = larfb_ws_doubles(m, n, QR_PANEL);
+  v.lfb_n = larfb_ws_doubles(m, n, QR_GROUP);
   v.bt_n = build_t_ws_doubles(m, n);
   v.Yh = take(v.ldm * n);
   v.Yq = take(v.ldm * n);

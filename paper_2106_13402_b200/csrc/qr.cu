@@ -83,14 +83,22 @@ int orgqr(Mat Y, Mat T, Mat Q, double* ws, size_t ws_doubles, cudaStream_t st) {
 // ---------------------------------------------------------------------------
 // K3/K4: blocked Householder QR.
 // ---------------------------------------------------------------------------
+// side stream scratch of one group factorisation: the intra-group larfb
+// (B = rows x QR_PANEL, w = QR_PANEL) and the local T merge temporaries
+static size_t side_ws_doubles(int rows) {
+  return larfb_ws_doubles(rows, qr::PANEL, qr::PANEL) + 2 * (size_t)qr::PANEL * qr::PANEL + 1024;
+}
+
 size_t geqrf_ws_doubles(int rows, int cols, bool /*want_t*/) {
   // taller than the fused panel kernel accepts: TSQR + reconstruction (tsqr.cu)
   if (rows > panel_rows_max())
     return 4096 + tsqr_ws_doubles(rows, cols, 1, panel_rows_max()) +
            (size_t)round_up(cols, 4) * cols + reconstruct_ws_doubles(cols);
-  // fused panel QR scratch + merge temporaries + trailing larfb workspace
+  // fused panel QR scratch + merge temporaries + trailing larfb workspace +
+  // the look-ahead side stream's private larfb / merge scratch
   return 4096 + sumsq_scratch_doubles() + panel_ws_doubles() +
-         2 * (size_t)round_up(cols, 4) * qr::PANEL + larfb_ws_doubles(rows, cols, qr::PANEL);
+         2 * (size_t)round_up(cols, 4) * QR_GROUP + larfb_ws_doubles(rows, cols, QR_GROUP) +
+         side_ws_doubles(rows);
 }
 
 // T[:j0, j0:j0+jb] = -T[:j0,:j0] (Y[j0:, :j0]^T Y[j0:, j0:j0+jb]) T[j0.., j0..]
@@ -108,25 +116,77 @@ static int merge_t(Mat Y, Mat T, int j0, int jb, double* S1, double* S2, double*
   return UTV_OK;
 }
 
-// Right-looking blocked QR over QR_PANEL-wide panels (each one fused
-// panel_qr launch), K = 256 DMMA trailing updates, optional T merges.
-// Look-ahead: the trailing update of panel j is split into the next panel's
-// columns (narrow) and the rest (wide); panel j+1 is factored on a
+// Factor the columns [g0, g0 + gw) (they already hold every earlier
+// group's update): QR_PANEL-wide fused panels, each first updated by the
+// group's earlier panels (K = QR_PANEL); whenever a panel completes a
+// QR_GROUP-aligned pair, the pair's T is merged locally
+// (T12 = -T1 (Y1^T Y2) T2), so T's QR_GROUP-wide diagonal blocks are always
+// complete whatever the update granularity.  Runs on stream s with a CTA
+// budget.
+static int factor_group(Mat P, Mat Y, Mat T, int g0, int gw, const double* fro2, double* pws,
+                        double* sws, cudaStream_t s, int ctas) {
+  const int rows = P.rows;
+  const size_t lfb_n = larfb_ws_doubles(rows, qr::PANEL, qr::PANEL);
+  double* S1 = sws + lfb_n;
+  double* S2 = S1 + (size_t)qr::PANEL * qr::PANEL;
+  double* gws = sws + (lfb_n - SPLITK_WS);
+  gemm_set_max_ctas(ctas);
+  int rc = UTV_OK;
+  for (int p0 = g0; p0 < g0 + gw && rc == UTV_OK; p0 += qr::PANEL) {
+    const int pw = min(qr::PANEL, g0 + gw - p0);
+    if (p0 > 0) rc = set_zero(Y.at(0, p0), Y.ld, p0, pw, s);
+    if (rc == UTV_OK && p0 > g0)
+      rc = larfb('L', true, Y.sub(g0, g0, rows - g0, p0 - g0), T.sub(g0, g0, p0 - g0, p0 - g0),
+                 P.sub(g0, p0, rows - g0, pw), sws, lfb_n, s);
+    if (rc == UTV_OK)
+      rc = panel_qr(P.sub(p0, p0, rows - p0, pw), Y.sub(p0, p0, rows - p0, pw), T.sub(p0, p0, pw, pw),
+                    fro2, pws, s, ctas);
+    const int q0 = p0 - qr::PANEL;  // the pair [q0, p0 + pw) is QR_GROUP-aligned
+    if (rc == UTV_OK && p0 % QR_GROUP == qr::PANEL)
+      rc = merge_t(Y.sub(q0, q0, rows - q0, qr::PANEL + pw), T.sub(q0, q0, qr::PANEL + pw, qr::PANEL + pw),
+                   qr::PANEL, pw, S1, S2, gws, s);
+  }
+  gemm_set_max_ctas(0);
+  return rc;
+}
+
+// Update granularity of the blocked QR (QR_PANEL or QR_GROUP columns per
+// trailing update; tuning knob UTV_QR_GROUP) and of the panel-blocked
+// applies (UTV_APPLY_GROUP).  Both default to QR_GROUP.
+static int env_group(const char* name) {
+  const char* e = getenv(name);
+  const int v = e ? atoi(e) : QR_GROUP;
+  return v == qr::PANEL ? qr::PANEL : QR_GROUP;
+}
+static int qr_group() {
+  static const int g = env_group("UTV_QR_GROUP");
+  return g;
+}
+static int apply_group() {
+  static const int g = env_group("UTV_APPLY_GROUP");
+  return g;
+}
+
+// Right-looking blocked QR over QR_GROUP-wide groups of QR_PANEL-wide fused
+// panels, K = QR_GROUP DMMA trailing updates, optional T merges.
+// Look-ahead: the trailing update of group j is split into the next group's
+// columns (narrow) and the rest (wide); group j+1 is factored on a
 // high-priority side stream (on <= 48 SMs) while the wide update runs on the
-// others, taking the latency-bound panel off the critical path.
+// others, taking the latency-bound panels off the critical path.
 static int geqrf_blocked(Mat P, Mat Y, Mat T, bool want_t, const double* fro2, Arena& ar,
                          cudaStream_t st) {
-  const int rows = P.rows, cols = P.cols, blk = qr::PANEL;
+  const int rows = P.rows, cols = P.cols, grp = qr_group();
   double* pws = ar.take(panel_ws_doubles());
-  double* S1 = ar.take((size_t)round_up(cols, 4) * blk);
-  double* S2 = ar.take((size_t)round_up(cols, 4) * blk);
-  const size_t lfb_n = larfb_ws_doubles(rows, cols, blk);
+  double* S1 = ar.take((size_t)round_up(cols, 4) * grp);
+  double* S2 = ar.take((size_t)round_up(cols, 4) * grp);
+  double* sws = ar.take(side_ws_doubles(rows));
+  const size_t lfb_n = larfb_ws_doubles(rows, cols, grp);
   double* lfb = ar.take(lfb_n);
   if (!lfb) return UTV_ERR_WORKSPACE;
   double* gws = lfb + (lfb_n - SPLITK_WS);
   cudaStream_t sa = nullptr;
   cudaEvent_t ev_narrow = nullptr, ev_panel = nullptr;
-  const bool lookahead = cols > blk;
+  const bool lookahead = cols > grp;
   if (lookahead) {
     UTV_CHECK(aux_stream_for(st, 1, &sa));
     UTV_CHECK(aux_event_for(st, 4, &ev_narrow));
@@ -138,41 +198,37 @@ static int geqrf_blocked(Mat P, Mat Y, Mat T, bool want_t, const double* fro2, A
     return v > 0 ? v : 48;
   }();
   static const int LA_ADAPT = [] {
-    const char* e = getenv("UTV_LA_ADAPT");  // tuning knob: wide width below which the panel gets all SMs
+    const char* e = getenv("UTV_LA_ADAPT");  // tuning knob: wide width below which the group gets all SMs
     return e ? atoi(e) : 0;
   }();
-  bool factored = false;  // panel j0 already factored (look-ahead) on sa
-  for (int j0 = 0; j0 < cols; j0 += blk) {
-    const int jb = cols - j0 < blk ? cols - j0 : blk;
-    Mat Yp = Y.sub(j0, j0, rows - j0, jb);
-    Mat Tp = T.sub(j0, j0, jb, jb);
+  bool factored = false;  // group g0 already factored (look-ahead) on sa
+  for (int g0 = 0; g0 < cols; g0 += grp) {
+    const int gw = cols - g0 < grp ? cols - g0 : grp;
+    Mat Yg = Y.sub(g0, g0, rows - g0, gw);
+    Mat Tg = T.sub(g0, g0, gw, gw);
     if (factored) {
       UTV_CUDA(cudaStreamWaitEvent(st, ev_panel, 0));
     } else {
-      if (j0 > 0) UTV_CHECK(set_zero(Y.at(0, j0), Y.ld, j0, jb, st));
-      UTV_CHECK(panel_qr(P.sub(j0, j0, rows - j0, jb), Yp, Tp, fro2, pws, st));
+      UTV_CHECK(factor_group(P, Y, T, g0, gw, fro2, pws, sws, st, 0));
     }
     factored = false;
-    const int j1 = j0 + jb;
-    if (j1 < cols) {
-      const int jb1 = cols - j1 < blk ? cols - j1 : blk;
-      Mat Bn = P.sub(j0, j1, rows - j0, jb1);
-      UTV_CHECK(larfb('L', true, Yp, Tp, Bn, lfb, lfb_n, st));
-      if (j1 + jb1 < cols) {
-        // panel j+1 on the side stream, the wide update on the main stream
+    const int g1 = g0 + gw;
+    if (g1 < cols) {
+      const int gw1 = cols - g1 < grp ? cols - g1 : grp;
+      UTV_CHECK(larfb('L', true, Yg, Tg, P.sub(g0, g1, rows - g0, gw1), lfb, lfb_n, st));
+      if (g1 + gw1 < cols) {
+        // group j+1 on the side stream, the wide update on the main stream
         UTV_CUDA(cudaEventRecord(ev_narrow, st));
         UTV_CUDA(cudaStreamWaitEvent(sa, ev_narrow, 0));
-        UTV_CHECK(set_zero(Y.at(0, j1), Y.ld, j1, jb1, sa));
-        UTV_CHECK(panel_qr(P.sub(j1, j1, rows - j1, jb1), Y.sub(j1, j1, rows - j1, jb1),
-                           T.sub(j1, j1, jb1, jb1), fro2, pws, sa,
-                           (cols - j1 - jb1) < LA_ADAPT ? 0 : LA_CTAS));
+        UTV_CHECK(factor_group(P, Y, T, g1, gw1, fro2, pws, sws, sa,
+                               (cols - g1 - gw1) < LA_ADAPT ? 0 : LA_CTAS));
         UTV_CUDA(cudaEventRecord(ev_panel, sa));
         factored = true;
-        UTV_CHECK(larfb('L', true, Yp, Tp, P.sub(j0, j1 + jb1, rows - j0, cols - j1 - jb1), lfb,
+        UTV_CHECK(larfb('L', true, Yg, Tg, P.sub(g0, g1 + gw1, rows - g0, cols - g1 - gw1), lfb,
                         lfb_n, st));
       }
     }
-    if (want_t) UTV_CHECK(merge_t(Y, T, j0, jb, S1, S2, gws, st));
+    if (want_t) UTV_CHECK(merge_t(Y, T, g0, gw, S1, S2, gws, st));
   }
   return UTV_OK;
 }
@@ -180,12 +236,12 @@ static int geqrf_blocked(Mat P, Mat Y, Mat T, bool want_t, const double* fro2, A
 int larfb_panels(char side, bool trans, Mat Y, Mat T, Mat B, double* ws, size_t ws_doubles,
                  cudaStream_t st) {
   const int k = Y.rows, w = Y.cols;
-  const int np = (w + qr::PANEL - 1) / qr::PANEL;
+  const int np = (w + apply_group() - 1) / apply_group();
   // forward order for B Q and Q^T B, reverse for B Q^T and Q B
   const bool fwd = (side == 'R') != trans;
   for (int jj = 0; jj < np; ++jj) {
     const int j = fwd ? jj : np - 1 - jj;
-    const int j0 = j * qr::PANEL, jb = (w - j0 < qr::PANEL) ? w - j0 : qr::PANEL;
+    const int j0 = j * apply_group(), jb = (w - j0 < apply_group()) ? w - j0 : apply_group();
     Mat Yj = Y.sub(j0, j0, k - j0, jb), Tj = T.sub(j0, j0, jb, jb);
     if (side == 'R')
       UTV_CHECK(larfb('R', trans, Yj, Tj, B.sub(0, j0, B.rows, k - j0), ws, ws_doubles, st));
@@ -198,9 +254,9 @@ int larfb_panels(char side, bool trans, Mat Y, Mat T, Mat B, double* ws, size_t 
 int orgqr_panels(Mat Y, Mat T, Mat Q, double* ws, size_t ws_doubles, cudaStream_t st) {
   const int m = Y.rows, w = Y.cols, nc = Q.cols;
   UTV_CHECK(set_identity(Q.p, Q.ld, m, nc, st));
-  const int np = (w + qr::PANEL - 1) / qr::PANEL;
+  const int np = (w + apply_group() - 1) / apply_group();
   for (int j = np - 1; j >= 0; --j) {
-    const int j0 = j * qr::PANEL, jb = (w - j0 < qr::PANEL) ? w - j0 : qr::PANEL;
+    const int j0 = j * apply_group(), jb = (w - j0 < apply_group()) ? w - j0 : apply_group();
     if (j0 >= nc) continue;  // Q_j leaves the leading columns of I untouched
     UTV_CHECK(larfb('L', false, Y.sub(j0, j0, m - j0, jb), T.sub(j0, j0, jb, jb),
                     Q.sub(j0, j0, m - j0, nc - j0), ws, ws_doubles, st));
@@ -262,7 +318,7 @@ int geqrf(Mat P, Mat Y, Mat Tw, bool want_t, double* ws, size_t ws_doubles, cuda
   if (!red) return UTV_ERR_WORKSPACE;
   UTV_CHECK(sumsq(P.p, P.ld, P.rows, P.cols, fro2, red, st));
   UTV_CHECK(set_zero(Tw.p, Tw.ld, P.cols, P.cols, st));
-  // want_t == false still delivers complete QR_PANEL-wide diagonal blocks of
+  // want_t == false still delivers complete QR_GROUP-wide diagonal blocks of
   // T (what larfb_panels / orgqr_panels / build_t consume).
   return geqrf_blocked(P, Y, Tw, want_t, fro2, ar, st);
 }

@@ -113,4 +113,26 @@ int aux_event(int idx, cudaEvent_t* e) {
   return UTV_OK;
 }
 
+// ---- process model guards ----
+// The library binds to the first device it is used on (side streams, events,
+// tile-scheduler slots, split-K turn counters and kernel attributes live on
+// it): entry points called with another current device fail with
+// UTV_ERR_DEVICE instead of touching foreign memory.
+namespace {
+std::once_flag g_dev_once;
+int g_dev = -1;
+std::mutex g_driver_mu;
+}  // namespace
+
+int check_device() {
+  int d = -1;
+  if (cudaGetDevice(&d) != cudaSuccess) return UTV_ERR_CUDA;
+  std::call_once(g_dev_once, [d] { g_dev = d; });
+  return d == g_dev ? UTV_OK : UTV_ERR_DEVICE;
+}
+
+// Drivers that use the shared side streams/events enqueue under this lock, so
+// concurrent host threads cannot interleave their record/wait pairs.
+std::mutex& driver_mutex() { return g_driver_mu; }
+
 }  // namespace utv

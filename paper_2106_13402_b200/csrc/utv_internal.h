@@ -22,6 +22,13 @@ int aux_event_for(cudaStream_t key, int idx, cudaEvent_t* e);
 // events 6-7: powerURV side build_t.
 int aux_stream_low(cudaStream_t* s);
 
+// ---- process model (streams.cu) ----
+int check_device();          // UTV_ERR_DEVICE if the current device is not the bound one
+}  // namespace utv
+#include <mutex>
+namespace utv {
+std::mutex& driver_mutex();  // serialises the side-stream drivers' enqueue
+
 // ---- launch accounting / profiling (prof.cu) ----
 enum ProfCat {
   PROF_GEMM = 0,      // DMMA GEMM kernel (flops = 2MNK)
@@ -131,10 +138,15 @@ int larfb(char side, bool trans, Mat Y, Mat T, Mat B, double* ws, size_t ws_doub
 int orgqr(Mat Y, Mat T, Mat Q, double* ws, size_t ws_doubles, cudaStream_t st);
 
 // Panel-blocked variants: Q = Q_1 Q_2 ... Q_p with Q_j = I - Y_j T_j Y_j^T,
-// T_j the QR_PANEL-wide diagonal blocks of T (off-diagonal blocks unused).
+// T_j the QR_GROUP-wide diagonal blocks of T (off-diagonal blocks unused).
 // Cost 2*rows*w*k-ish instead of the dense-T 3-GEMM form (no w x w x rows
 // middle product, no full T needed).
 constexpr int QR_PANEL = 256;
+// Compact-WY block width of the blocked QR's trailing updates and of the
+// panel-blocked applies: two QR_PANEL panels whose T is merged locally
+// (the K = 512 update GEMMs amortise the DMMA GEMM's per-tile cost twice as
+// well as K = 256).  geqrf always delivers complete QR_GROUP diagonal blocks.
+constexpr int QR_GROUP = 512;
 int larfb_panels(char side, bool trans, Mat Y, Mat T, Mat B, double* ws, size_t ws_doubles,
                  cudaStream_t st);
 int orgqr_panels(Mat Y, Mat T, Mat Q, double* ws, size_t ws_doubles, cudaStream_t st);

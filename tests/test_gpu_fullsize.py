@@ -102,6 +102,21 @@ def test_randutv_fp32_c5_fullsize():
     rel = reconstruction_device(a64, u64, t64, v64)
     print("C5 reconstruction", rel)
     assert rel < 1e-4
+    # e_k (Frobenius, from T) against Eckart-Young of the known spectrum
+    # (svd.py:85-100, bench.py:63-72; SURVEY §8c C5 criterion)
+    from paper_2106_13402_b200.metrics import trailing_fro_curve_device
+    e = trailing_fro_curve_device(t64)
+    d = 10.0 ** (-3.0 * np.arange(r) / (r - 1))
+    tail = np.sqrt(np.cumsum((d ** 2)[::-1])[::-1])            # ||d[k:]||_2, k = 0..r-1
+    ey = np.concatenate([tail[1:], np.zeros(n - r)])[: n - 1]  # e_opt(k), k = 1..n-1
+    fro = float(tail[0])
+    slack = 1e-5 * fro                                         # fp32 sampling / storage noise
+    assert np.all(e >= ey - slack), "e_k below the Eckart-Young floor"
+    ks = np.arange(1, r)
+    ratio = e[ks - 1] / ey[ks - 1]
+    assert np.mean(ratio <= 2.0) >= 0.9, np.percentile(ratio, [50, 90, 99])
+    assert e[r + b - 1:].max() < 1e-4 * fro                   # past the rank: fp32 noise
+    print("C5 e_k/EY median", float(np.median(ratio)), "p90", float(np.percentile(ratio, 90)))
     # the trailing block past the rank is fp32 noise
     tt = t64.t[r + b:, r + b:n]
     assert (tt.norm() / a64.t[:n, :n].norm()).item() < 1e-4

@@ -246,3 +246,21 @@ def test_geqrf_writes_stay_inside_the_view(rows, cols):
     E[:cols] = torch.eye(cols, device="cuda", dtype=torch.float64)
     Q = E - Yd @ (Td @ Yd[:cols].T)
     assert ((Q @ Rd - A).abs().max() / A.abs().max()).item() < 1e-13
+
+
+def test_fused_splitk_matches_reduce_kernel_bitwise(tmp_path):
+    """The fused split-K epilogue (per-tile turn counters, splits summed in
+    split order, last split applies alpha/beta) gives the same bits as the
+    separate fixed-order reduce kernel (UTV_SPLITK_FUSE_MAX=0)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for tag, env in (("fused", {}), ("reduce", {"UTV_SPLITK_FUSE_MAX": "0"})):
+        path = str(tmp_path / f"{tag}.npz")
+        subprocess.run([sys.executable, os.path.join(root, "tools", "splitk_bits.py"), path],
+                       check=True, env={**os.environ, **env}, timeout=600)
+        outs[tag] = np.load(path)
+    for key in outs["fused"].files:
+        assert np.array_equal(outs["fused"][key], outs["reduce"][key]), key
