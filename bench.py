@@ -46,6 +46,12 @@ GEMM_TRAFFIC = {"bytes": 2.821095e9 + 2.106140e9, "algorithmic_bytes": 2 * 8 * 1
                 "launch": "dgemm NT M=N=16384 K=256 beta=1 (compact-WY trailing update)",
                 "source": "profiles/r01_ncu_gemm_nt_16384x16384x256_v4.txt"}
 FP64_PEAK_SRC = "measured: tools/fp64_peak.cu DMMA m8n8k4, 148 SMs @1965 MHz (profiles/fp64_peak_r01.json)"
+# dense TF32 tcgen05 peak (M=128, N=128 - K10's MMA shape), measured by
+# tools/tf32_peak.cu (profiles/tf32_peak_r02.json); 3xTF32 does 3 MMAs per
+# useful product, so the useful-FLOP roofline of K10 is a third of it
+TF32_PEAK_TFLOPS = 1061.5
+TF32_PEAK_SRC = ("measured: tools/tf32_peak.cu tcgen05.mma.cta_group::1.kind::tf32 M=128 N=128, "
+                 "148 SMs @1965 MHz (profiles/tf32_peak_r02.json); useful peak = 1/3 (3xTF32)")
 
 
 # ---------------------------------------------------------------------------
@@ -820,8 +826,13 @@ def run_c5(args):
             "config": {"workload": f"C5 randUTV b={b} q={q} fp32 on {n}x{n}, rank {r}",
                        "l2_policy": "inputs (4 GiB) larger than L2",
                        "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
-            "roofline": {"kernel": "sgemm_tf32x3_kernel (tcgen05.mma kind::tf32, 3 products)",
-                         "achieved_useful_tflops": g["flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else 0.0,
+            "roofline": {"bound": "tensor",
+                         "kernel": "sgemm_tf32x3_kernel (tcgen05.mma kind::tf32, 3 products)",
+                         "achieved": g["flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else 0.0,
+                         "peak": TF32_PEAK_TFLOPS / 3, "unit": "TFLOP/s (useful)",
+                         "frac": (g["flops"] / (g["ms"] / 1e3) / 1e12) / (TF32_PEAK_TFLOPS / 3)
+                         if g["ms"] > 0 else 0.0,
+                         "peak_source": TF32_PEAK_SRC, "traffic": None,
                          "share_of_step": g["ms"] / 1e3 / per},
             "phase_ms": {k: round(v["ms"], 3) for k, v in prof.items()},
             "gpu_launches": int(launches), "clocks": clk, "e2e": None, "cpu_baseline": None}

@@ -777,8 +777,11 @@ int dgemm_ex(bool ta, bool tb, int M, int N, int K, double alpha, const double* 
   // running CTA -> no deadlock), the per-tile sums fit the workspace
   // tile-major, and the serial chain of S epilogues stays short.
   static const int fuse_max = [] {
-    const char* e = getenv("UTV_SPLITK_FUSE_MAX");  // tuning knob (0 = always the reduce kernel)
-    return e ? atoi(e) : 4;
+    // tuning knob, default 0 = the separate reduce kernel: the serial chain
+    // of S epilogues measured slower than one reduce launch (TN 256x16384x16384:
+    // 33.5 -> 32.3 TF/s; headline step +35 ms in randUTV, profiles/r02_ab_groups.txt)
+    const char* e = getenv("UTV_SPLITK_FUSE_MAX");
+    return e ? atoi(e) : 0;
   }();
   a.flags = nullptr;
   if (splits > 1 && splits <= fuse_max && a.sched && tm * tn <= FLAG_TILES &&

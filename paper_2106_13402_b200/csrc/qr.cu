@@ -116,6 +116,27 @@ static int merge_t(Mat Y, Mat T, int j0, int jb, double* S1, double* S2, double*
   return UTV_OK;
 }
 
+// Update granularity of the blocked QR (QR_PANEL or QR_GROUP columns per
+// trailing update; tuning knob UTV_QR_GROUP) and of the panel-blocked
+// applies (UTV_APPLY_GROUP).  Both default to QR_PANEL: the K = 512 update
+// GEMMs run 7% faster (32 vs 30 TF/s, tools/gemm_ab.py), but the wider
+// look-ahead group (two panels + their inner update on 48 SMs) and the
+// 512-wide middle products cost more than that in powerURV
+// (profiles/r02_ab_groups.txt: 2.997 s at 256/256 vs 3.118 s at 512/512).
+static int env_group(const char* name) {
+  const char* e = getenv(name);
+  const int v = e ? atoi(e) : qr::PANEL;
+  return v == QR_GROUP ? QR_GROUP : qr::PANEL;
+}
+static int qr_group() {
+  static const int g = env_group("UTV_QR_GROUP");
+  return g;
+}
+static int apply_group() {
+  static const int g = env_group("UTV_APPLY_GROUP");
+  return g;
+}
+
 // Factor the columns [g0, g0 + gw) (they already hold every earlier
 // group's update): QR_PANEL-wide fused panels, each first updated by the
 // group's earlier panels (K = QR_PANEL); whenever a panel completes a
@@ -142,29 +163,12 @@ static int factor_group(Mat P, Mat Y, Mat T, int g0, int gw, const double* fro2,
       rc = panel_qr(P.sub(p0, p0, rows - p0, pw), Y.sub(p0, p0, rows - p0, pw), T.sub(p0, p0, pw, pw),
                     fro2, pws, s, ctas);
     const int q0 = p0 - qr::PANEL;  // the pair [q0, p0 + pw) is QR_GROUP-aligned
-    if (rc == UTV_OK && p0 % QR_GROUP == qr::PANEL)
+    if (rc == UTV_OK && p0 % QR_GROUP == qr::PANEL && (qr_group() == QR_GROUP || apply_group() == QR_GROUP))
       rc = merge_t(Y.sub(q0, q0, rows - q0, qr::PANEL + pw), T.sub(q0, q0, qr::PANEL + pw, qr::PANEL + pw),
                    qr::PANEL, pw, S1, S2, gws, s);
   }
   gemm_set_max_ctas(0);
   return rc;
-}
-
-// Update granularity of the blocked QR (QR_PANEL or QR_GROUP columns per
-// trailing update; tuning knob UTV_QR_GROUP) and of the panel-blocked
-// applies (UTV_APPLY_GROUP).  Both default to QR_GROUP.
-static int env_group(const char* name) {
-  const char* e = getenv(name);
-  const int v = e ? atoi(e) : QR_GROUP;
-  return v == qr::PANEL ? qr::PANEL : QR_GROUP;
-}
-static int qr_group() {
-  static const int g = env_group("UTV_QR_GROUP");
-  return g;
-}
-static int apply_group() {
-  static const int g = env_group("UTV_APPLY_GROUP");
-  return g;
 }
 
 // Right-looking blocked QR over QR_GROUP-wide groups of QR_PANEL-wide fused

@@ -142,10 +142,10 @@ int orgqr(Mat Y, Mat T, Mat Q, double* ws, size_t ws_doubles, cudaStream_t st);
 // Cost 2*rows*w*k-ish instead of the dense-T 3-GEMM form (no w x w x rows
 // middle product, no full T needed).
 constexpr int QR_PANEL = 256;
-// Compact-WY block width of the blocked QR's trailing updates and of the
-// panel-blocked applies: two QR_PANEL panels whose T is merged locally
-// (the K = 512 update GEMMs amortise the DMMA GEMM's per-tile cost twice as
-// well as K = 256).  geqrf always delivers complete QR_GROUP diagonal blocks.
+// Optional wider compact-WY block for the blocked QR's trailing updates and
+// the panel-blocked applies (UTV_QR_GROUP / UTV_APPLY_GROUP = 512): two
+// QR_PANEL panels whose T is merged locally.  Measured slower end to end,
+// so both default to QR_PANEL (qr.cu).
 constexpr int QR_GROUP = 512;
 int larfb_panels(char side, bool trans, Mat Y, Mat T, Mat B, double* ws, size_t ws_doubles,
                  cudaStream_t st);

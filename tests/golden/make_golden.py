@@ -217,8 +217,32 @@ def rsvd():
     print("wrote rsvd_gauss60x40.npz")
 
 
+def spec_acc5():
+    """SPEC acceptance 5 as the reference computes it (the REF_ACC5 table in
+    tests/test_gpu_spec.py): max_k e_k/sigma_{k+1} - 1 (spectral) of
+    randutv_boosted(q=2, p=b) and randutv_basic(q=2), n=400, b=50, on
+    gen_fast_decay(400, 1e-5, RngStream(200 + 10 s)), s = 0..4."""
+    sys.dont_write_bytecode = True
+    sys.path.insert(0, REF)
+    import utvkit as uk  # noqa: E402
+
+    def curve(t):
+        r = min(t.shape)
+        return np.array([np.linalg.svd(t[k:r, k:], compute_uv=False)[0] if k < r else 0.0
+                         for k in range(1, t.shape[1])])
+    for s in range(5):
+        seed = 200 + 10 * s
+        a, sig = uk.gen_fast_decay(400, 1e-5, uk.RngStream(seed))
+        opt = np.sort(sig)[::-1][1:]
+        cb = curve(uk.randutv_boosted(a, 50, 2, 50, uk.RngStream(seed + 1)).T)
+        cs = curve(uk.randutv_basic(a, 50, 2, uk.RngStream(seed + 1)).T)
+        print(f"({np.max(cb / opt - 1)!r}, {np.max(cs / opt - 1)!r}),")
+
+
 if __name__ == "__main__":
-    if len(sys.argv) > 1 and sys.argv[1] == "rsvd":
+    if len(sys.argv) > 1 and sys.argv[1] == "spec_acc5":
+        spec_acc5()
+    elif len(sys.argv) > 1 and sys.argv[1] == "rsvd":
         rsvd()
     elif len(sys.argv) > 1 and sys.argv[1] == "hqrcp":
         hqrcp()

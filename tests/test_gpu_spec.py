@@ -115,7 +115,7 @@ def test_acceptance4_5_7_error_curves(kind):
             # the values are the reference's: utvkit itself gives
             # (rel_boosted, rel_basic) = (0.12410, 0.17815), (0.12634, 0.15252),
             # (0.11331, 0.19558), (0.12264, 0.16049), (0.21769, 0.14803) on
-            # these five matrices (run in the build container)
+            # these five matrices (tests/golden/make_golden.py spec_acc5)
             ref = REF_ACC5[seed]
             assert abs(rel_b - ref[0]) < 1e-6 and abs(rel_basic - ref[1]) < 1e-6, (seed, rel_b, rel_basic)
     if kind == "fast":
