@@ -119,6 +119,8 @@ int utv_dlaset(char uplo, int m, int n, double alpha, double beta, double* A, lo
                void* stream);
 int utv_ddiag_scale(char side, int m, int n, const double* d, double alpha, double* A, long lda,
                     void* stream);
+/* bytes of device memory <- 0 on the stream (status / mass vectors). */
+int utv_zero(void* p, size_t bytes, void* stream);
 /* FP32 dlaset (identity / zero initialisation of the fp32 randUTV's U, V). */
 int utv_slaset(char uplo, int m, int n, float alpha, float beta, float* A, long lda, void* stream);
 /* *flag (device int) <- 1 if any entry of the m x n block is NaN or +-Inf,

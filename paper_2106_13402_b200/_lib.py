@@ -84,6 +84,7 @@ SIGNATURES = {
     "utv_slaset": (c_int, [c_char, c_int, c_int, ctypes.c_float, ctypes.c_float, c_void_p, c_long,
                            c_void_p]),
     "utv_dnonfinite": (c_int, [c_int, c_int, c_void_p, c_long, c_void_p, c_void_p]),
+    "utv_zero": (c_int, [c_void_p, c_size_t, c_void_p]),
     "utv_dtri_zero": (c_int, [c_char, c_int, c_int, c_void_p, c_long, c_void_p]),
     "utv_dtranspose": (c_int, [c_int, c_int, c_void_p, c_long, c_void_p, c_long, c_void_p]),
     "utv_dgen_bie": (c_int, [c_int, c_void_p, c_long, c_void_p]),
@@ -453,6 +454,14 @@ def _laset(m, alpha, beta):
     check(load().utv_dlaset(b"A", m.rows, m.cols, alpha, beta, m.ptr, m.ld, stream_ptr()),
           "utv_dlaset")
     return m
+
+
+def dzero_vec(n, dtype=None):
+    """n zeros on the device (cudaMemsetAsync through utv_zero, no torch kernel)."""
+    torch = torch_cuda()
+    v = torch.empty(max(int(n), 1), dtype=torch.float64 if dtype is None else dtype, device="cuda")
+    check(load().utv_zero(v.data_ptr(), v.numel() * v.element_size(), stream_ptr()), "utv_zero")
+    return v[: int(n)] if n else v[:0]
 
 
 def dzeros(rows, cols):

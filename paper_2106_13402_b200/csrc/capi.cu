@@ -240,6 +240,12 @@ int utv_slaset(char uplo, int m, int n, float alpha, float beta, float* A, long 
   return laset_f32(u, m, n, alpha, beta, A, lda, S(stream));
 }
 
+int utv_zero(void* p, size_t bytes, void* stream) {
+  if (bytes && !p) return -1;
+  if (bytes) UTV_CUDA(cudaMemsetAsync(p, 0, bytes, S(stream)));
+  return UTV_OK;
+}
+
 int utv_dnonfinite(int m, int n, const double* A, long lda, int* flag, void* stream) {
   if (m < 0) return -1;
   if (n < 0) return -2;

@@ -72,6 +72,7 @@ struct Args {
   // semaphore says z's turn; the last split applies alpha/beta to C.  Same
   // summation order as the separate reduce kernel -> the same bits.
   int* flags;  // per-tile turn counters (self-resetting), null = separate reduce kernel
+  int wstore;  // HASC: per-warp TMA stores of the C tile (tmCw, 16 x 32 boxes)
 };
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -139,7 +140,8 @@ template <bool TA, bool TB, bool HASC>
 __global__ void __launch_bounds__(THREADS, 1)
     dgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA,
                      const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmC, const Args p) {
+                     const __grid_constant__ CUtensorMap tmC,
+                     const __grid_constant__ CUtensorMap tmCw, const Args p) {
   constexpr int STAGES = Cfg<HASC>::STAGES;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte alignment (128B swizzle atoms) by offsetting the shared pointer
@@ -153,6 +155,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t full0 = smem_u32(bars);
   const uint32_t empty0 = smem_u32(bars + STAGES);
   const uint32_t cfull = smem_u32(bars + 2 * STAGES);
+  // every warp done with the smem C tile (its TMA stores have read it): the
+  // next tile's C may be prefetched over it (per-warp epilogue, p.wstore)
+  const uint32_t cempty = smem_u32(bars + 2 * STAGES + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ktot = p.K + p.k_sh;
@@ -174,6 +179,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(empty0 + 8 * s, NCW);
     }
     mbar_init(cfull, 1);
+    mbar_init(cempty, NCW);
     fence_barrier_init();
   }
   __syncthreads();
@@ -425,7 +431,33 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
     }
-    if (HASC) {
+    if (HASC && p.wstore) {
+      // per-warp epilogue: each warp stores its own 64 x 32 sub-tile with
+      // four 16 x 32 TMA boxes as soon as IT has written them — no CTA
+      // barrier, so the other warps are already into the next tile's main
+      // loop; thread 0 prefetches the next C tile once all eight warps'
+      // stores have read sC (cempty).
+      if (tstore) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int rg = wm * 4 + i;  // 16-row group of this warp
+            tma_store_2d(&tmCw, smem_u32(sC + rg * 16 * BN + wn * 32 * 16), m0 + 16 * rg, n0 + 32 * wn);
+          }
+          bulk_commit();
+          bulk_wait_read0();
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(cempty);
+      if (threadIdx.x == 0) {
+        mbar_wait(cempty, (uint32_t)(local & 1));
+        const int nxt = tq[(local + 1) & 7];
+        if (nxt >= 0 && p.beta != 0.0) load_c(nxt);
+      }
+    } else if (HASC) {
       if (tstore) fence_proxy_async_smem();  // generic smem writes -> async proxy
       __syncthreads();  // every warp is done with sC
       if (threadIdx.x == 0) {
@@ -440,7 +472,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   }
-  if (HASC && threadIdx.x == 0) bulk_wait0();
+  if (HASC && (threadIdx.x == 0 || (p.wstore && lane == 0))) bulk_wait0();
 }
 
 // C = alpha * sum_s ws[s] + beta * C, summed in split order (deterministic).
@@ -750,6 +782,16 @@ int dgemm_ex(bool ta, bool tb, int M, int N, int K, double alpha, const double* 
     UTV_CHECK(make_map(&mC, C, M, N, ldc, 16, gemm::BN, &c_sh));
     if (c_sh != a_sh) hasc = false;
   }
+  // per-warp C stores (16 x 32 boxes of the same swizzled smem tile)
+  static const bool wstore = [] {
+    const char* e = getenv("UTV_GEMM_WSTORE");  // tuning knob (0 = one CTA-wide TMA store)
+    return e ? atoi(e) != 0 : true;
+  }();
+  CUtensorMap mCw = mC;
+  if (hasc && wstore) {
+    int c_sh2 = 0;
+    UTV_CHECK(make_map(&mCw, C, M, N, ldc, 16, 32, &c_sh2));
+  }
   // beta != 0 with a C map of the wrong parity (odd offsets only): route
   // through the split-K workspace path (one split) + the reduce kernel.
   double* ctmp = nullptr;
@@ -783,6 +825,7 @@ int dgemm_ex(bool ta, bool tb, int M, int N, int K, double alpha, const double* 
     const char* e = getenv("UTV_SPLITK_FUSE_MAX");
     return e ? atoi(e) : 0;
   }();
+  a.wstore = (hasc && wstore) ? 1 : 0;
   a.flags = nullptr;
   if (splits > 1 && splits <= fuse_max && a.sched && tm * tn <= FLAG_TILES &&
       (size_t)tm * tn * gemm::BM * gemm::BN <= ws_doubles)
@@ -808,16 +851,16 @@ int dgemm_ex(bool ta, bool tb, int M, int N, int K, double alpha, const double* 
   ProfScope ps(PROF_GEMM, fl, 8.0 * ((double)M * K + (double)K * N + (beta != 0.0 ? 2.0 : 1.0) * M * N), st);
   if (hasc) {
     const size_t sm = gemm::Cfg<true>::SMEM;
-    if (!ta && !tb) gemm::dgemm_tma_kernel<false, false, true><<<grid, gemm::THREADS, sm, st>>>(mA, mB, mC, a);
-    else if (!ta && tb) gemm::dgemm_tma_kernel<false, true, true><<<grid, gemm::THREADS, sm, st>>>(mA, mB, mC, a);
-    else if (ta && !tb) gemm::dgemm_tma_kernel<true, false, true><<<grid, gemm::THREADS, sm, st>>>(mA, mB, mC, a);
-    else gemm::dgemm_tma_kernel<true, true, true><<<grid, gemm::THREADS, sm, st>>>(mA, mB, mC, a);
+    if (!ta && !tb) gemm::dgemm_tma_kernel<false, false, true><<<grid, gemm::THREADS, sm, st>>>(mA, mB, mC, mCw, a);
+    else if (!ta && tb) gemm::dgemm_tma_kernel<false, true, true><<<grid, gemm::THREADS, sm, st>>>(mA, mB, mC, mCw, a);
+    else if (ta && !tb) gemm::dgemm_tma_kernel<true, false, true><<<grid, gemm::THREADS, sm, st>>>(mA, mB, mC, mCw, a);
+    else gemm::dgemm_tma_kernel<true, true, true><<<grid, gemm::THREADS, sm, st>>>(mA, mB, mC, mCw, a);
   } else {
     const size_t sm = gemm::Cfg<false>::SMEM;
-    if (!ta && !tb) gemm::dgemm_tma_kernel<false, false, false><<<grid, gemm::THREADS, sm, st>>>(mA, mB, mC, a);
-    else if (!ta && tb) gemm::dgemm_tma_kernel<false, true, false><<<grid, gemm::THREADS, sm, st>>>(mA, mB, mC, a);
-    else if (ta && !tb) gemm::dgemm_tma_kernel<true, false, false><<<grid, gemm::THREADS, sm, st>>>(mA, mB, mC, a);
-    else gemm::dgemm_tma_kernel<true, true, false><<<grid, gemm::THREADS, sm, st>>>(mA, mB, mC, a);
+    if (!ta && !tb) gemm::dgemm_tma_kernel<false, false, false><<<grid, gemm::THREADS, sm, st>>>(mA, mB, mC, mCw, a);
+    else if (!ta && tb) gemm::dgemm_tma_kernel<false, true, false><<<grid, gemm::THREADS, sm, st>>>(mA, mB, mC, mCw, a);
+    else if (ta && !tb) gemm::dgemm_tma_kernel<true, false, false><<<grid, gemm::THREADS, sm, st>>>(mA, mB, mC, mCw, a);
+    else gemm::dgemm_tma_kernel<true, true, false><<<grid, gemm::THREADS, sm, st>>>(mA, mB, mC, mCw, a);
   }
   UTV_CUDA(cudaGetLastError());
   }

@@ -48,7 +48,7 @@ def sgemm_tf32x3(transa, transb, alpha, A: DMat, B: DMat, beta=0.0, C: DMat | No
 def sumsq(A: DMat):
     import torch
     lib = load()
-    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    out = _lib.dzero_vec(1, torch.float64)
     lw = lib.utv_dsumsq_bufsize()
     ws = workspace(lw)
     check(lib.utv_dsumsq(A.rows, A.cols, A.ptr, A.ld, out.data_ptr(), ws.data_ptr(), lw,
@@ -118,7 +118,7 @@ def gesvj(A: DMat):
     sig = torch.empty(max(n, 1), dtype=torch.float64, device="cuda")
     U = dempty(n, n)
     V = dempty(n, n)
-    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    status = _lib.dzero_vec(1, torch.int32)
     lw = lib.utv_dgesvj_bufsize(n)
     ws = workspace(lw)
     check(lib.utv_dgesvj(n, A.ptr, A.ld, sig.data_ptr(), U.ptr, U.ld, V.ptr, V.ld,
@@ -155,9 +155,9 @@ class RandUtvRun:
         self.ws = workspace(self.lw)
         steps = -(-n // b)
         self.steps = steps
-        self.errsq = torch.zeros(steps, dtype=torch.float64, device="cuda")
-        self.trail2 = torch.zeros(steps, dtype=torch.float64, device="cuda") if record_trailing else None
-        self.status = torch.zeros(steps, dtype=torch.int32, device="cuda")
+        self.errsq = _lib.dzero_vec(steps, torch.float64)
+        self.trail2 = _lib.dzero_vec(steps, torch.float64) if record_trailing else None
+        self.status = _lib.dzero_vec(steps, torch.int32)
 
     def run(self, T: DMat, U: DMat, V: DMat, G: DMat):
         lib = load()
@@ -179,9 +179,9 @@ class RandUtvRun32:
         self.ws = workspace(self.lw)
         steps = -(-n // b)
         self.steps = steps
-        self.errsq = torch.zeros(steps, dtype=torch.float64, device="cuda")
-        self.trail2 = torch.zeros(steps, dtype=torch.float64, device="cuda") if record_trailing else None
-        self.status = torch.zeros(steps, dtype=torch.int32, device="cuda")
+        self.errsq = _lib.dzero_vec(steps, torch.float64)
+        self.trail2 = _lib.dzero_vec(steps, torch.float64) if record_trailing else None
+        self.status = _lib.dzero_vec(steps, torch.int32)
 
     def run(self, T: DMat, U: DMat, V: DMat, G: DMat):
         lib = load()

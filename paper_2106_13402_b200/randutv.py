@@ -208,9 +208,9 @@ def _randutv_stepwise(a, b, q, p, rng, boosted, tol_fro=None, max_rank=None,
     t_dev = dfrom_numpy(a)
     U, V = deye(m), deye(n)
     steps_max = -(-n // b)
-    errsq = torch.zeros(steps_max, dtype=torch.float64, device="cuda")
-    trail2 = torch.zeros(steps_max, dtype=torch.float64, device="cuda") if record_trailing else None
-    status = torch.zeros(steps_max, dtype=torch.int32, device="cuda")
+    errsq = _lib.dzero_vec(steps_max, torch.float64)
+    trail2 = _lib.dzero_vec(steps_max, torch.float64) if record_trailing else None
+    status = _lib.dzero_vec(steps_max, torch.int32)
     lw = lib.utv_randutv_step_bufsize(m, n, b, pe, q)
     ws = _lib.workspace(lw)
     carried, is_final = ctypes.c_int(0), ctypes.c_int(0)
