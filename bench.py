@@ -684,7 +684,7 @@ def run_c4(args, nested=False):
     torch.cuda.synchronize()
 
     def step():
-        return sharded.power_urv_sharded_native(a, g, q, comm)
+        return sharded.power_urv_sharded_native(a, g, q, comm, chunk_rows=args.c4_chunk or None)
 
     for _ in range(warmup):
         out = step()
@@ -709,7 +709,7 @@ def run_c4(args, nested=False):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (device N(0,1) rows per rank; G from the reference PCG64 stream)",
             "config": {"workload": f"C4 powerURV q={q} on {m}x{n} fp64, row-sharded over {ws} rank(s)",
-                       "rows_per_rank": rows,
+                       "rows_per_rank": rows, "tsqr_leaf_rows": args.c4_chunk or "panel limit",
                        "parallelism": f"row shards x{ws} (utv_powerurv_sharded_f64: NCCL allgather "
                                       f"+ allreduce + broadcast inside libutvb200)" if ws > 1
                                       else "1 GPU (utv_powerurv_sharded_f64, 1-rank communicator)",
@@ -881,6 +881,8 @@ def main():
     ap.add_argument("--c5-rank", type=int, default=2000)
     ap.add_argument("--c4-rows", type=int, default=524288)
     ap.add_argument("--c4-cols", type=int, default=4096)
+    ap.add_argument("--c4-chunk", type=int, default=0,
+                    help="TSQR leaf rows (0 = the panel kernel's limit, 75776)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(_spawn_ranks(args.gpus))
