@@ -197,9 +197,9 @@ static int geqrf_blocked(Mat P, Mat Y, Mat T, bool want_t, const double* fro2, A
     UTV_CHECK(aux_event_for(st, 5, &ev_panel));
   }
   static const int LA_CTAS = [] {
-    const char* e = getenv("UTV_LA_CTAS");  // tuning knob (default 48)
+    const char* e = getenv("UTV_LA_CTAS");  // tuning knob (default 64, profiles/r02_la_sweep.txt)
     const int v = e ? atoi(e) : 0;
-    return v > 0 ? v : 48;
+    return v > 0 ? v : 64;
   }();
   static const int LA_ADAPT = [] {
     const char* e = getenv("UTV_LA_ADAPT");  // tuning knob: wide width below which the group gets all SMs
