@@ -235,6 +235,26 @@ int utv_powerurv_f64_yhat(int m, int n, int q, const double* A, long lda, const 
                           long ldr, double* Vy, long ldvy, double* Vt, long ldvt, void* work,
                           size_t lwork, void* stream, void* vq_ready, void* r_ready);
 
+/* powerURV with progressive results: G (or, for q >= 1, Yhat0 = A G instead
+ * of G — pass the other as NULL) and ncols_ev = ceil(n / 256) events per
+ * array (each array may be NULL).  r_cols[j] is recorded once columns
+ * [256 j, 256 j + 256) of R and Uq.Y are final — during the final QR,
+ * panel by panel — and t_cols[j] once the same columns of Uq.Twy are: the
+ * dense triangle's column blocks are merged on a low-priority side stream
+ * as the panels complete (powerurv.py:70-71 + qr.py:63-68), so a caller can
+ * copy every output out while the factorisation still runs.  vq_ready as
+ * in utv_powerurv_f64_ev.  progress_cb (optional, void cb(void* ctx, int
+ * kind, int index)) is called on the calling host thread right after each
+ * progress event's record has been ENQUEUED (kind 0: vq_ready, 1: r_cols[index],
+ * 2: t_cols[index]): the launch queue holds the calling thread for most of
+ * the device run, so copy jobs must be handed to another thread from there. */
+int utv_powerurv_f64_cols(int m, int n, int q, const double* A, long lda, const double* G, long ldg,
+                          const double* Yhat0, long ldy0, double* Uy, long lduy, double* Ut,
+                          long ldut, double* R, long ldr, double* Vy, long ldvy, double* Vt,
+                          long ldvt, void* work, size_t lwork, void* stream, void* vq_ready,
+                          int ncols_ev, void* const* r_cols, void* const* t_cols,
+                          void* progress_cb, void* progress_ctx);
+
 /* ---- Row-sharded powerURV over several GPUs (BASELINE C4) ----
  * The reference has no multi-GPU path (powerurv.py:41-72 is one process);
  * this is its SPMD form: one process (or, for emulation, one host thread)

@@ -72,6 +72,11 @@ SIGNATURES = {
                                    c_void_p, c_long, c_void_p, c_long, c_void_p, c_long, c_void_p,
                                    c_long, c_void_p, c_long, c_void_p, c_size_t, c_void_p,
                                    c_void_p, c_void_p]),
+    "utv_powerurv_f64_cols": (c_int, [c_int, c_int, c_int, c_void_p, c_long, c_void_p, c_long,
+                                      c_void_p, c_long, c_void_p, c_long, c_void_p, c_long, c_void_p,
+                                      c_long, c_void_p, c_long, c_void_p, c_long, c_void_p, c_size_t,
+                                      c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p,
+                                      c_void_p]),
     "utv_dgeqrf_rows_max": (c_int, []),
     "utv_dgeqp3_bufsize": (c_size_t, [c_int, c_int]),
     "utv_dgeqp3_max_dim": (c_int, []),
@@ -347,6 +352,10 @@ def d2h_numpy(m):
     return out
 
 
+_D2H_TRACE = bool(os.environ.get("UTV_D2H_TRACE"))
+_D2H_T0 = __import__("time").perf_counter()
+
+
 class AsyncD2H:
     """Background device->host copies of column blocks that are FINAL (no
     later kernel writes them): each job waits (on the device) for an event
@@ -418,6 +427,13 @@ class AsyncD2H:
                 continue
             event, blocks = job
             try:
+                # wait for the producing kernels on the host BEFORE taking the
+                # shared ring: a job whose data is not final yet must not
+                # hold the ring (and every other copy) while it waits
+                event.synchronize()
+                if _D2H_TRACE:
+                    import time
+                    t1 = time.perf_counter()
                 with torch.cuda.stream(self.stream):
                     self.stream.wait_event(event)
                     for m, host, c0, c1 in blocks:
@@ -430,6 +446,11 @@ class AsyncD2H:
                         self._wait_faults(host, c0 * m.rows * es, c1 * m.rows * es)
                         with _ASYNC_LOCK:
                             _d2h_bytes(src, dst, self.stream, self.ring, self.pool)
+                if _D2H_TRACE:
+                    t2 = time.perf_counter()
+                    nb = sum((c1 - c0) * m.rows * m.esize for m, _, c0, c1 in blocks)
+                    print(f"[d2h {id(self) % 1000:3d}] ready {t1 - _D2H_T0:.3f} copied {t2 - _D2H_T0:.3f} "
+                          f"{nb / 2**20:.0f} MiB {nb / max(t2 - t1, 1e-9) / 1e9:.1f} GB/s", flush=True)
             except BaseException as e:  # surfaced by finish()
                 self.err = e
 

@@ -26,7 +26,8 @@ int powerurv_sharded(Comm* comm, int m, int n, int q, Mat A, Mat G, Mat Uy, Mat 
                      Mat Vt, int cap, double* ws, size_t ws_doubles, cudaStream_t st);
 int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, Mat Vt, double* ws,
              size_t ws_doubles, cudaStream_t st, cudaEvent_t vq_ready, const double* yhat0 = nullptr,
-             long ldy0 = 0, cudaEvent_t r_ready = nullptr);
+             long ldy0 = 0, cudaEvent_t r_ready = nullptr, const cudaEvent_t* r_cols = nullptr,
+             const cudaEvent_t* t_cols = nullptr, ProgressFn cb = nullptr, void* cb_ctx = nullptr);
 }  // namespace utv
 
 using namespace utv;
@@ -436,6 +437,33 @@ int utv_powerurv_f64_yhat(int m, int n, int q, const double* A, long lda, const 
                   Mat{Uy, lduy, m, n}, Mat{Ut, ldut, n, n}, Mat{R, ldr, m, n}, Mat{Vy, ldvy, n, n},
                   Mat{Vt, ldvt, n, n}, (double*)work, lwork / sizeof(double), S(stream),
                   (cudaEvent_t)vq_ready, Yhat0, ldy0, (cudaEvent_t)r_ready);
+}
+
+int utv_powerurv_f64_cols(int m, int n, int q, const double* A, long lda, const double* G, long ldg,
+                          const double* Yhat0, long ldy0, double* Uy, long lduy, double* Ut,
+                          long ldut, double* R, long ldr, double* Vy, long ldvy, double* Vt,
+                          long ldvt, void* work, size_t lwork, void* stream, void* vq_ready,
+                          int ncols_ev, void* const* r_cols, void* const* t_cols,
+                          void* progress_cb, void* progress_ctx) {
+  if (m < 1) return -1;
+  if (n < 1 || n > m) return -2;
+  if (q < 0 || (Yhat0 && q < 1)) return -3;
+  if (!ld_ok(lda, m)) return -5;
+  if (!Yhat0 && (!G || !ld_ok(ldg, n))) return -7;
+  if (Yhat0 && !ld_ok(ldy0, m)) return -9;
+  if (!ld_ok(lduy, m)) return -11;
+  if (!ld_ok(ldut, n)) return -13;
+  if (!ld_ok(ldr, m)) return -15;
+  if (!ld_ok(ldvy, n)) return -17;
+  if (!ld_ok(ldvt, n)) return -19;
+  const int ngrp = (n + QR_PANEL - 1) / QR_PANEL;
+  if ((r_cols || t_cols) && ncols_ev != ngrp) return -24;
+  UTV_DRIVER_GUARD();
+  return powerurv(m, n, q, Mat{(double*)A, lda, m, n}, Mat{(double*)G, ldg, n, n},
+                  Mat{Uy, lduy, m, n}, Mat{Ut, ldut, n, n}, Mat{R, ldr, m, n}, Mat{Vy, ldvy, n, n},
+                  Mat{Vt, ldvt, n, n}, (double*)work, lwork / sizeof(double), S(stream),
+                  (cudaEvent_t)vq_ready, Yhat0, ldy0, nullptr, (const cudaEvent_t*)r_cols,
+                  (const cudaEvent_t*)t_cols, (ProgressFn)progress_cb, progress_ctx);
 }
 
 size_t utv_powerurv_sharded_bufsize(int m_local, int n, int nranks, int chunk_rows) {

@@ -23,7 +23,6 @@
 namespace utv {
 
 namespace jac {
-constexpr int WMAX = 16;          // columns per block (16 for n <= 400, 8 up to 800, 4 beyond)
 constexpr int MAX_SWEEPS = 40;
 constexpr double EPS = 2.220446049250313e-16;
 

@@ -57,6 +57,20 @@ static size_t plan_purv(int m, int n, PurvWs* w, double* base) {
 
 size_t powerurv_ws_doubles(int m, int n) { return plan_purv(m, n, nullptr, nullptr); }
 
+// Library-owned per-panel progress events for the final QR when the caller
+// passes none (drivers enqueue under the driver lock, so one pool suffices).
+static const cudaEvent_t* progress_events(int n) {
+  constexpr int MAXG = 256;
+  static cudaEvent_t pool[MAXG];
+  static int made = 0;
+  if (n > MAXG) return nullptr;
+  while (made < n) {
+    if (cudaEventCreateWithFlags(&pool[made], cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    ++made;
+  }
+  return pool;
+}
+
 // vq_ready (optional): recorded once Vq (Y and the dense T) is final, so the
 // caller can start copying it out while A Q(Vq) and the final QR run.
 // r_ready (optional): recorded once R and Uq.Y are final (before Uq's dense
@@ -64,9 +78,14 @@ size_t powerurv_ws_doubles(int m, int n) { return plan_purv(m, n, nullptr, nullp
 // yhat0 (optional, q >= 1): the caller already formed Yhat = A G (e.g. as
 // K-chunked products while G was still being drawn on the host); G is then
 // not read.
+// r_cols / t_cols (optional, ceil(n / QR_PANEL) events each): r_cols[j] is
+// recorded once columns [j*256, (j+1)*256) of R and Uq.Y are final (during
+// the final QR), t_cols[j] once the same columns of Uq's dense triangle are
+// (merged on the low-priority stream while the final QR still runs).
 int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, Mat Vt, double* ws,
              size_t ws_doubles, cudaStream_t st, cudaEvent_t vq_ready, const double* yhat0,
-             long ldy0, cudaEvent_t r_ready) {
+             long ldy0, cudaEvent_t r_ready, const cudaEvent_t* r_cols, const cudaEvent_t* t_cols,
+             ProgressFn cb, void* cb_ctx) {
   if (m < n) return -1;
   if (q < 0) return -3;
   if (ws_doubles < plan_purv(m, n, nullptr, nullptr)) return UTV_ERR_WORKSPACE;
@@ -84,6 +103,10 @@ int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, M
     pname[np++] = name;
   };
   mark("start");
+  static const int BT_SIDE = [] {
+    const char* e = getenv("UTV_PURV_BT_SIDE");  // tuning knob; 0 = in stream order
+    return e ? atoi(e) : 64;
+  }();
   cudaStream_t sb = nullptr;
   cudaEvent_t ev_bt0 = nullptr, ev_bt1 = nullptr;
   bool bt_side = false;
@@ -92,6 +115,7 @@ int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, M
     UTV_CHECK(copy_mat(G.p, G.ld, w.Yn, w.ldn, n, n, st));
     UTV_CHECK(geqrf(Mat{w.Yn, w.ldn, n, n}, Vy, Vt, true, w.qr, w.qr_n, st));
     if (vq_ready) UTV_CUDA(cudaEventRecord(vq_ready, st));
+    if (vq_ready && cb) cb(cb_ctx, 0, 0);
   } else {
     // Neither Vhat nor the next round's V is ever formed: with Q the
     // Householder QR of Yhat, Y = A^T Vhat = ((Q^T A)[:n, :])^T, and
@@ -129,10 +153,6 @@ int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, M
     // on a low-priority side stream (CTA budget) while A Q(Vq) — which reads
     // only the diagonal blocks — and the final QR run; it fills the SMs the
     // QR's latency-bound panels leave idle.
-    static const int BT_SIDE = [] {
-      const char* e = getenv("UTV_PURV_BT_SIDE");  // tuning knob; 0 = in stream order
-      return e ? atoi(e) : 64;
-    }();
     if (BT_SIDE > 0) {
       UTV_CHECK(aux_stream_low(&sb));
       UTV_CHECK(aux_event(6, &ev_bt0));
@@ -145,10 +165,12 @@ int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, M
       UTV_CHECK(rc);
       UTV_CUDA(cudaEventRecord(ev_bt1, sb));
       if (vq_ready) UTV_CUDA(cudaEventRecord(vq_ready, sb));
+      if (vq_ready && cb) cb(cb_ctx, 0, 0);
       bt_side = true;
     } else {
       UTV_CHECK(build_t(Vy, Vt, w.bt, w.bt_n, st));
       if (vq_ready) UTV_CUDA(cudaEventRecord(vq_ready, st));
+      if (vq_ready && cb) cb(cb_ctx, 0, 0);
     }
     mark("build_t(V)");
   }
@@ -156,13 +178,54 @@ int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, M
   UTV_CHECK(copy_mat(A.p, A.ld, R.p, R.ld, m, n, st));
   UTV_CHECK(larfb_panels('R', false, Vy, Vt, R, w.lfb, w.lfb_n, st));
   mark("A*Q(V)");
-  // (Uq, R) = hqr_full(Ahat) (powerurv.py:71)
-  UTV_CHECK(geqrf(R, Uy, Ut, false, w.qr, w.qr_n, st));
-  mark("geqrf(Ahat)");
-  if (r_ready) UTV_CUDA(cudaEventRecord(r_ready, st));  // R and Uq.Y are final; Uq.Twy follows
-  if (bt_side) UTV_CUDA(cudaStreamWaitEvent(st, ev_bt1, 0));  // w.bt reused below
-  UTV_CHECK(build_t(Uy, Ut, w.bt, w.bt_n, st));
-  mark("build_t(U)");
+  // (Uq, R) = hqr_full(Ahat) (powerurv.py:71).  Uq's dense triangle: each
+  // off-diagonal column block T[:j0, j0:j0+256] needs only Y's columns
+  // < j0 + 256, so the merges run on the low-priority side stream as the
+  // final QR's panels complete (per-panel events) instead of after it, and
+  // column blocks of R, Uq.Y and Uq.Twy become final (copyable) progressively.
+  // Progressive merges on the side stream measured slower (they compete
+  // with the final QR's critical path: powerURV 2.94 -> 3.01 s at n=16384),
+  // so by default the triangle is built after the QR (tuning knob
+  // UTV_PURV_PROG_T=1 enables them); the per-panel r_cols events still let
+  // R and Uq.Y stream out during the QR.
+  static const bool prog_t = [] {
+    const char* e = getenv("UTV_PURV_PROG_T");
+    return e ? atoi(e) != 0 : false;
+  }();
+  const int ngrp = (n + QR_PANEL - 1) / QR_PANEL;
+  const cudaEvent_t* evr = r_cols;
+  if (prog_t && bt_side && !evr) evr = progress_events(ngrp);
+  if (prog_t && bt_side && evr) {
+    UTV_CHECK(geqrf_ev(R, Uy, Ut, false, w.qr, w.qr_n, st, evr, r_cols ? cb : nullptr, cb_ctx, 1));
+    mark("geqrf(Ahat)");
+    if (r_ready) UTV_CUDA(cudaEventRecord(r_ready, st));
+    gemm_set_max_ctas(BT_SIDE);
+    int rc = UTV_OK;
+    for (int g = 0; g < ngrp && rc == UTV_OK; ++g) {
+      const int j0 = g * QR_PANEL, jb = min(QR_PANEL, n - j0);
+      if (cudaStreamWaitEvent(sb, evr[g], 0) != cudaSuccess) rc = UTV_ERR_CUDA;
+      if (rc == UTV_OK && j0 > 0) rc = merge_t_block(Uy, Ut, j0, jb, w.bt, w.bt_n, sb);
+      if (rc == UTV_OK && t_cols && cudaEventRecord(t_cols[g], sb) != cudaSuccess) rc = UTV_ERR_CUDA;
+      if (rc == UTV_OK && t_cols && cb) cb(cb_ctx, 2, g);
+    }
+    gemm_set_max_ctas(0);
+    UTV_CHECK(rc);
+    UTV_CUDA(cudaEventRecord(ev_bt1, sb));
+    UTV_CUDA(cudaStreamWaitEvent(st, ev_bt1, 0));  // the call completes on st
+    mark("build_t(U) side");
+  } else {
+    UTV_CHECK(geqrf_ev(R, Uy, Ut, false, w.qr, w.qr_n, st, r_cols, cb, cb_ctx, 1));
+    mark("geqrf(Ahat)");
+    if (r_ready) UTV_CUDA(cudaEventRecord(r_ready, st));  // R and Uq.Y are final; Uq.Twy follows
+    if (bt_side) UTV_CUDA(cudaStreamWaitEvent(st, ev_bt1, 0));  // w.bt reused below
+    UTV_CHECK(build_t(Uy, Ut, w.bt, w.bt_n, st));
+    if (t_cols)
+      for (int g = 0; g < ngrp; ++g) {
+        UTV_CUDA(cudaEventRecord(t_cols[g], st));
+        if (cb) cb(cb_ctx, 2, g);
+      }
+    mark("build_t(U)");
+  }
   if (phases) {
     cudaEventSynchronize(pev[np - 1]);
     for (int i = 1; i < np; ++i) {

@@ -177,8 +177,13 @@ static int factor_group(Mat P, Mat Y, Mat T, int g0, int gw, const double* fro2,
 // columns (narrow) and the rest (wide); group j+1 is factored on a
 // high-priority side stream (on <= 48 SMs) while the wide update runs on the
 // others, taking the latency-bound panels off the critical path.
+// grp_ev (optional, one per QR_PANEL columns): recorded on st as soon as the
+// columns of that panel are final in P (R) and Y — their panel is factored
+// and every earlier group's update has reached them — so the caller can
+// consume R / Y column blocks (copy them out, merge T) while the QR runs.
 static int geqrf_blocked(Mat P, Mat Y, Mat T, bool want_t, const double* fro2, Arena& ar,
-                         cudaStream_t st) {
+                         cudaStream_t st, const cudaEvent_t* grp_ev, ProgressFn cb, void* cb_ctx,
+                         int cb_kind) {
   const int rows = P.rows, cols = P.cols, grp = qr_group();
   double* pws = ar.take(panel_ws_doubles());
   double* S1 = ar.take((size_t)round_up(cols, 4) * grp);
@@ -216,6 +221,11 @@ static int geqrf_blocked(Mat P, Mat Y, Mat T, bool want_t, const double* fro2, A
       UTV_CHECK(factor_group(P, Y, T, g0, gw, fro2, pws, sws, st, 0));
     }
     factored = false;
+    if (grp_ev)
+      for (int p0 = g0; p0 < g0 + gw; p0 += qr::PANEL) {
+        UTV_CUDA(cudaEventRecord(grp_ev[p0 / qr::PANEL], st));
+        if (cb) cb(cb_ctx, cb_kind, p0 / qr::PANEL);
+      }
     const int g1 = g0 + gw;
     if (g1 < cols) {
       const int gw1 = cols - g1 < grp ? cols - g1 : grp;
@@ -268,6 +278,16 @@ int orgqr_panels(Mat Y, Mat T, Mat Q, double* ws, size_t ws_doubles, cudaStream_
   return UTV_OK;
 }
 
+int merge_t_block(Mat Y, Mat T, int j0, int jb, double* ws, size_t ws_doubles, cudaStream_t st) {
+  const int cols = Y.cols;
+  Arena ar{(char*)ws, ws_doubles * sizeof(double), 0};
+  double* S1 = ar.take((size_t)round_up(cols, 4) * qr::PANEL);
+  double* S2 = ar.take((size_t)round_up(cols, 4) * qr::PANEL);
+  double* gws = ar.take(SPLITK_WS);
+  if (!gws) return UTV_ERR_WORKSPACE;
+  return merge_t(Y, T, j0, jb, S1, S2, gws, st);
+}
+
 size_t build_t_ws_doubles(int rows, int cols) {
   return 2 * (size_t)round_up(cols, 4) * qr::PANEL + SPLITK_WS + 1024;
 }
@@ -314,8 +334,21 @@ static int geqrf_tall(Mat P, Mat Y, Mat Tw, double* ws, size_t ws_doubles, cudaS
 }
 
 int geqrf(Mat P, Mat Y, Mat Tw, bool want_t, double* ws, size_t ws_doubles, cudaStream_t st) {
+  return geqrf_ev(P, Y, Tw, want_t, ws, ws_doubles, st, nullptr);
+}
+
+int geqrf_ev(Mat P, Mat Y, Mat Tw, bool want_t, double* ws, size_t ws_doubles, cudaStream_t st,
+             const cudaEvent_t* grp_ev, ProgressFn cb, void* cb_ctx, int cb_kind) {
   if (P.rows < P.cols) return -1;
-  if (P.rows > panel_rows_max()) return geqrf_tall(P, Y, Tw, ws, ws_doubles, st);
+  if (P.rows > panel_rows_max()) {
+    UTV_CHECK(geqrf_tall(P, Y, Tw, ws, ws_doubles, st));
+    if (grp_ev)  // TSQR: every column is final at the end
+      for (int p0 = 0; p0 < P.cols; p0 += qr::PANEL) {
+        UTV_CUDA(cudaEventRecord(grp_ev[p0 / qr::PANEL], st));
+        if (cb) cb(cb_ctx, cb_kind, p0 / qr::PANEL);
+      }
+    return UTV_OK;
+  }
   Arena ar{(char*)ws, ws_doubles * sizeof(double), 0};
   double* fro2 = ar.take(8);
   double* red = ar.take(sumsq_scratch_doubles());
@@ -324,7 +357,7 @@ int geqrf(Mat P, Mat Y, Mat Tw, bool want_t, double* ws, size_t ws_doubles, cuda
   UTV_CHECK(set_zero(Tw.p, Tw.ld, P.cols, P.cols, st));
   // want_t == false still delivers complete QR_GROUP-wide diagonal blocks of
   // T (what larfb_panels / orgqr_panels / build_t consume).
-  return geqrf_blocked(P, Y, Tw, want_t, fro2, ar, st);
+  return geqrf_blocked(P, Y, Tw, want_t, fro2, ar, st, grp_ev, cb, cb_ctx, cb_kind);
 }
 
 }  // namespace utv

@@ -128,6 +128,16 @@ void panel_set_max_ctas(int n);
 int panel_qr(Mat P, Mat Y, Mat T, const double* fro2, double* ws, cudaStream_t st,
              int max_ctas = 0);
 int geqrf(Mat P, Mat Y, Mat Tw, bool want_t, double* ws, size_t ws_doubles, cudaStream_t st);
+// The same, recording grp_ev[j] on st once columns [j*QR_PANEL, (j+1)*QR_PANEL)
+// of R (in P) and Y are final (grp_ev: ceil(cols / QR_PANEL) events).
+// Host progress callback of the streaming drivers: called right after the
+// cudaEventRecord of a progress event has been ENQUEUED (kind, index), so a
+// caller whose host thread is held by the launch queue can still hand copy
+// jobs to another thread in time.
+typedef void (*ProgressFn)(void* ctx, int kind, int index);
+int geqrf_ev(Mat P, Mat Y, Mat Tw, bool want_t, double* ws, size_t ws_doubles, cudaStream_t st,
+             const cudaEvent_t* grp_ev, ProgressFn cb = nullptr, void* cb_ctx = nullptr,
+             int cb_kind = 0);
 
 // ---- K2 compact-WY apply (qr.cu) ----
 // side 'L': B <- Q^(T) B ; side 'R': B <- B Q^(T);  Q = I - Y T Y^T, Y is k x w.
@@ -155,6 +165,8 @@ int orgqr_panels(Mat Y, Mat T, Mat Q, double* ws, size_t ws_doubles, cudaStream_
 // forward compact-WY triangle of the whole product (qr.py:63-68 semantics).
 size_t build_t_ws_doubles(int rows, int cols);
 int build_t(Mat Y, Mat T, double* ws, size_t ws_doubles, cudaStream_t st);
+// One off-diagonal column block of build_t: T[:j0, j0:j0+jb] (ws: build_t_ws_doubles).
+int merge_t_block(Mat Y, Mat T, int j0, int jb, double* ws, size_t ws_doubles, cudaStream_t st);
 
 // ---- column-pivoted QR comparator (qrcp.cu), qr.py:152-204 ----
 int qrcp_max_dim();

@@ -223,6 +223,35 @@ class PowerUrvRun:
             self.ws.data_ptr(), self.lw, stream_ptr(), self._ev(vq_event), self._ev(r_event)),
             "utv_powerurv_f64")
 
+    def run_cols(self, A: DMat, G: DMat | None = None, Yhat0: DMat | None = None, vq_event=None,
+                 r_events=None, t_events=None, progress=None):
+        """utv_powerurv_f64_cols: G, or (q >= 1) Yhat0 = A G; r_events[j] /
+        t_events[j] (torch.cuda.Event lists of ceil(n/256), optional) are
+        recorded once columns [256 j, 256 j + 256) of R and Uq.Y, resp. of
+        Uq.Twy, are final."""
+        import ctypes
+        lib = load()
+        ngrp = -(-self.n // 256)
+
+        def arr(evs):
+            if evs is None:
+                return None
+            assert len(evs) == ngrp
+            return (ctypes.c_void_p * ngrp)(*[self._ev(e) for e in evs])
+        ra, ta = arr(r_events), arr(t_events)
+        cb = None
+        if progress is not None:
+            proto = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int, ctypes.c_int)
+            cb = proto(lambda _ctx, kind, index: progress(kind, index))
+        check(lib.utv_powerurv_f64_cols(
+            self.m, self.n, self.q, A.ptr, A.ld, G.ptr if G is not None else None,
+            G.ld if G is not None else 2, Yhat0.ptr if Yhat0 is not None else None,
+            Yhat0.ld if Yhat0 is not None else 2, self.Uy.ptr, self.Uy.ld, self.Ut.ptr, self.Ut.ld,
+            self.R.ptr, self.R.ld, self.Vy.ptr, self.Vy.ld, self.Vt.ptr, self.Vt.ld,
+            self.ws.data_ptr(), self.lw, stream_ptr(), self._ev(vq_event), ngrp, ra, ta,
+            ctypes.cast(cb, ctypes.c_void_p) if cb is not None else None, None),
+            "utv_powerurv_f64_cols")
+
     def run_yhat(self, A: DMat, Yhat0: DMat, vq_event=None, r_event=None):
         """q >= 1 with the first product Yhat = A G already formed (utv_powerurv_f64_yhat)."""
         lib = load()
