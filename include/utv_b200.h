@@ -162,6 +162,13 @@ int utv_dorgqr(int m, int ncols, int w, const double* Y, long ldy, const double*
 size_t utv_dgesvj_bufsize(int n);
 int utv_dgesvj(int n, const double* A, long lda, double* sigma, double* U, long ldu, double* V,
                long ldv, int* status, void* work, size_t lwork, void* stream);
+/* The same with the rounds' orientation chosen explicitly: transpose = 1
+ * runs the rotations on A^T (the default of utv_dgesvj: fewer rotations on
+ * randUTV's graded triangles), 0 on A (columns of A itself: the convergence
+ * test then measures A's own column orthogonality — what the blocked
+ * Jacobi of svd_dense beyond n = 1024 needs), -1 the default. */
+int utv_dgesvj_ex(int n, const double* A, long lda, double* sigma, double* U, long ldu, double* V,
+                  long ldv, int* status, int transpose, void* work, size_t lwork, void* stream);
 
 /* Blocked randUTV, basic variant (randutv_basic, randutv.py:228-235 ->
  * _randutv 110-182, _sample_basic 185-193).

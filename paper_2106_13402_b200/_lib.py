@@ -43,6 +43,8 @@ SIGNATURES = {
     "utv_dgesvj_bufsize": (c_size_t, [c_int]),
     "utv_dgesvj": (c_int, [c_int, c_void_p, c_long, c_void_p, c_void_p, c_long, c_void_p, c_long,
                            c_void_p, c_void_p, c_size_t, c_void_p]),
+    "utv_dgesvj_ex": (c_int, [c_int, c_void_p, c_long, c_void_p, c_void_p, c_long, c_void_p, c_long,
+                              c_void_p, c_int, c_void_p, c_size_t, c_void_p]),
     "utv_randutv_basic_bufsize": (c_size_t, [c_int, c_int, c_int, c_int]),
     "utv_randutv_basic_f64": (c_int, [c_int, c_int, c_int, c_int, c_void_p, c_long, c_void_p,
                                       c_long, c_void_p, c_long, c_void_p, c_long, c_void_p,

@@ -366,6 +366,17 @@ int utv_dgesvj(int n, const double* A, long lda, double* sigma, double* U, long 
                (double*)work, lwork / sizeof(double), status, S(stream));
 }
 
+int utv_dgesvj_ex(int n, const double* A, long lda, double* sigma, double* U, long ldu, double* V,
+                  long ldv, int* status, int transpose, void* work, size_t lwork, void* stream) {
+  if (n < 1 || n > 1024) return -1;
+  if (lda < n) return -3;
+  if (ldu < n) return -6;
+  if (ldv < n) return -8;
+  if (transpose < -1 || transpose > 1) return -10;
+  return gesvj_ex(Mat{(double*)A, lda, n, n}, sigma, Mat{U, ldu, n, n}, Mat{V, ldv, n, n},
+                  (double*)work, lwork / sizeof(double), status, S(stream), transpose);
+}
+
 size_t utv_randutv_basic_bufsize(int m, int n, int b, int) { return B(randutv_ws_doubles(m, n, b)); }
 
 int utv_randutv_basic_f64(int m, int n, int b, int q, double* T, long ldt, double* U, long ldu,

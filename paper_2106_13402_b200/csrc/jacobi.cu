@@ -326,6 +326,12 @@ static bool g_jac_attr = false;
 
 int gesvj(Mat A, double* sigma, Mat U, Mat V, double* ws, size_t ws_doubles, int* status_dev,
           cudaStream_t st) {
+  return gesvj_ex(A, sigma, U, V, ws, ws_doubles, status_dev, st, -1);
+}
+
+// orient: -1 = the default (UTV_JAC_TRANSPOSE, on), 0 = rounds on A, 1 = on A^T.
+int gesvj_ex(Mat A, double* sigma, Mat U, Mat V, double* ws, size_t ws_doubles, int* status_dev,
+             cudaStream_t st, int orient) {
   const int n = A.rows;
   if (n <= 0) return UTV_OK;
   if (n > 1024) return -1;
@@ -347,10 +353,11 @@ int gesvj(Mat A, double* sigma, Mat U, Mat V, double* ws, size_t ws_doubles, int
   // block 6.2 -> 2.8 ms, tools/jacobi_transpose_probe.py).  A^T = W S X^T
   // gives A = X S W^T: the outputs swap (U <- normalised columns, with the
   // null-column completion, goes to V; W goes to U) and the sign rule reads V.
-  static const bool tr = [] {
+  static const bool tr_default = [] {
     const char* e = getenv("UTV_JAC_TRANSPOSE");
     return e ? atoi(e) != 0 : true;
   }();
+  const bool tr = orient < 0 ? tr_default : orient != 0;
   UTV_CHECK(set_zero(Aw, ld, (int)ld, (int)npad, st));
   if (tr) UTV_CHECK(transpose(A.p, A.ld, Aw, ld, n, n, st));
   else UTV_CHECK(copy_mat(A.p, A.ld, Aw, ld, n, n, st));

@@ -218,12 +218,19 @@ int powerurv(int m, int n, int q, Mat A, Mat G, Mat Uy, Mat Ut, Mat R, Mat Vy, M
     mark("geqrf(Ahat)");
     if (r_ready) UTV_CUDA(cudaEventRecord(r_ready, st));  // R and Uq.Y are final; Uq.Twy follows
     if (bt_side) UTV_CUDA(cudaStreamWaitEvent(st, ev_bt1, 0));  // w.bt reused below
-    UTV_CHECK(build_t(Uy, Ut, w.bt, w.bt_n, st));
-    if (t_cols)
+    if (t_cols) {
+      // build_t's merges one column block at a time (the same kernels, in
+      // the same order), each block's event recorded as soon as it is final:
+      // the cheap early blocks leave the GPU while the later merges run
       for (int g = 0; g < ngrp; ++g) {
+        const int j0 = g * QR_PANEL, jb = min(QR_PANEL, n - j0);
+        if (j0 > 0) UTV_CHECK(merge_t_block(Uy, Ut, j0, jb, w.bt, w.bt_n, st));
         UTV_CUDA(cudaEventRecord(t_cols[g], st));
         if (cb) cb(cb_ctx, 2, g);
       }
+    } else {
+      UTV_CHECK(build_t(Uy, Ut, w.bt, w.bt_n, st));
+    }
     mark("build_t(U)");
   }
   if (phases) {

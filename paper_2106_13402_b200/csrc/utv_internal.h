@@ -189,6 +189,9 @@ size_t lu_ws_doubles();
 size_t gesvj_ws_doubles(int n);
 int gesvj(Mat A, double* sigma, Mat U, Mat V, double* ws, size_t ws_doubles, int* status_dev,
           cudaStream_t st);
+// transpose: -1 default (rounds on A^T), 0 on A, 1 on A^T
+int gesvj_ex(Mat A, double* sigma, Mat U, Mat V, double* ws, size_t ws_doubles, int* status_dev,
+             cudaStream_t st, int transpose);
 
 // ---- communicators (comm.cu): collectives on FP64 device buffers, caller's stream ----
 struct Comm {

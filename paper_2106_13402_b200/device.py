@@ -110,8 +110,9 @@ def orgqr(Y: DMat, T: DMat, ncols):
     return Q
 
 
-def gesvj(A: DMat):
-    """Returns (sigma tensor, U, V, status tensor)."""
+def gesvj(A: DMat, transpose=None):
+    """Returns (sigma tensor, U, V, status tensor).  transpose: None = the
+    library default (rounds on A^T), False / True = on A / on A^T."""
     import torch
     lib = load()
     n = A.rows
@@ -121,8 +122,13 @@ def gesvj(A: DMat):
     status = _lib.dzero_vec(1, torch.int32)
     lw = lib.utv_dgesvj_bufsize(n)
     ws = workspace(lw)
-    check(lib.utv_dgesvj(n, A.ptr, A.ld, sig.data_ptr(), U.ptr, U.ld, V.ptr, V.ld,
-                         status.data_ptr(), ws.data_ptr(), lw, stream_ptr()), "utv_dgesvj")
+    if transpose is None:
+        check(lib.utv_dgesvj(n, A.ptr, A.ld, sig.data_ptr(), U.ptr, U.ld, V.ptr, V.ld,
+                             status.data_ptr(), ws.data_ptr(), lw, stream_ptr()), "utv_dgesvj")
+    else:
+        check(lib.utv_dgesvj_ex(n, A.ptr, A.ld, sig.data_ptr(), U.ptr, U.ld, V.ptr, V.ld,
+                                status.data_ptr(), 1 if transpose else 0, ws.data_ptr(), lw,
+                                stream_ptr()), "utv_dgesvj_ex")
     return sig, U, V, status
 
 
