@@ -429,8 +429,52 @@ def kernel_entries(prof, step_s, n, b, q, sweeps):
                    "sweeps_max": int(np.max(sweeps)) if len(sweeps) else None},
         "splitk_reduce": {"ms_per_step": sk["ms"], "launches": sk["count"],
                           "share_of_step": sk["ms"] / 1e3 / step_s},
+        "note": "panel_qr / jacobi ms are event intervals on their launching streams inside "
+                "the step: the Jacobi SVDs run on a side stream sharing SMs with the GEMMs, "
+                "so see 'isolated' for the kernels timed alone",
     }
     return out
+
+
+def isolated_kernels(n_panel=16384, b=256, reps=3):
+    """The two latency-bound kernels timed alone (CUDA events, after warm-up):
+    one fused panel QR of an n_panel x b panel, and one b x b Jacobi SVD of a
+    graded upper triangle (the R of a panel QR of a decaying matrix, what
+    randUTV hands the SVD)."""
+    import torch
+    import paper_2106_13402_b200.device as dv
+    from paper_2106_13402_b200._lib import dempty, dfrom_numpy
+
+    def ev_time(fn):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+    rng = np.random.default_rng(0)
+    p0 = dfrom_numpy(rng.standard_normal((n_panel, b)) * np.logspace(0, -5, b))
+    work = dempty(n_panel, b)
+
+    def panel():
+        dv.lacpy(p0, work)
+        dv.geqrf(work)
+    t_panel = ev_time(panel)
+    t_copy = ev_time(lambda: dv.lacpy(p0, work))
+    dv.lacpy(p0, work)
+    dv.geqrf(work)
+    r = dempty(b, b)
+    dv.lacpy(work.sub(0, 0, b, b), r)
+    t_jac = ev_time(lambda: dv.gesvj(r))
+    sweeps = int(dv.gesvj(r)[3].cpu().item())
+    ms_panel = t_panel - t_copy
+    return {"panel_qr": {"shape": f"{n_panel}x{b}", "call": "utv_dgeqrf (panel kernel + T)", "ms": ms_panel,
+                         "us_per_column": 1e3 * ms_panel / b,
+                         "algorithmic_GBps": 8.0 * 3 * n_panel * b / (ms_panel / 1e3) / 1e9},
+            "jacobi": {"shape": f"{b}x{b} graded triangle", "ms_per_call": t_jac, "sweeps": sweeps}}
 
 
 def run_ours(args, nested=False):
@@ -573,7 +617,8 @@ def run_ours(args, nested=False):
                                         "intervals over all streams (CUDA events, live)",
                      "sum_of_launch_ms": g["ms"],
                      "launches_per_step": g["count"]},
-        "kernels": kernel_entries(prof, rutv_s + purv_s, n, b, q, sweeps),
+        "kernels": dict(kernel_entries(prof, rutv_s + purv_s, n, b, q, sweeps),
+                        isolated=isolated_kernels(n, b) if not nested else None),
         "phase_ms": phase,
         "jacobi_sweeps": {"mean": float(np.mean(sweeps)), "max": int(np.max(sweeps))},
         "gpu_launches": int(launches),

@@ -9,28 +9,55 @@
 //     V column is positive (svd.py:53-57)
 //   * exactly zero block -> U = V = I (gesdd behaviour)
 //
-// B200 design: block one-sided Jacobi.  Columns are split into 2G blocks of
-// W=16; a cooperative grid of G CTAs processes the G block pairs of one
-// round-robin round concurrently (each pair resident in shared memory, one
-// warp per column pair, warp-shuffle dot products), then grid-syncs.  A and
-// the accumulated V live in an L2-resident workspace between rounds.  A
-// second kernel forms sigma, sorts, normalises U = A V / sigma, completes
-// null columns of U by CGS2 against the standard basis, and applies the sign
-// rule.
+// B200 design: block one-sided Jacobi in Gram form.  Columns are split into
+// 2P blocks of 16; every round of the circle-method tournament a thread-block
+// cluster of C CTAs owns one block pair, CTA r holding a slice of R = ne / C
+// rows of the pair's 32 columns of A and V in shared memory.  The cluster
+// forms the pair's 32 x 32 Gram matrix (partials summed over DSMEM), runs the
+// rotation sub-rounds on it (one warp per rotation, no dot products), and
+// applies the accumulated 32 x 32 rotation to its A and V rows; A and V live
+// in an L2-resident workspace between rounds (grid barrier).  The rounds were
+// smem-bandwidth bound when every rotation re-read and rewrote both columns
+// (tools/jacobi_probe.cu: 1.76 us per sub-round at n = 256).  A second kernel
+// forms sigma, sorts, normalises U = A V / sigma, completes null columns of U
+// by CGS2 against the standard basis, and applies the sign rule.
 #include "common.cuh"
 #include "utv_internal.h"
 
 namespace utv {
 
 namespace jac {
+// Diagnostics: build with -DJAC_PROBE (tools/jacobi_probe.cu) to accumulate
+// CTA 0's per-phase %globaltimer durations into g_probe.
+#ifdef JAC_PROBE
+__device__ unsigned long long g_probe[8];
+__device__ unsigned long long g_probe2[8];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+  return v;
+}
+#define JPROBE(k)                                  \
+  if (blockIdx.x == 0 && threadIdx.x == 0) {       \
+    const unsigned long long now_ = gtime();       \
+    g_probe[k] += now_ - probe_last;               \
+    probe_last = now_;                             \
+  }
+#else
+#define JPROBE(k)
+#endif
 constexpr int MAX_SWEEPS = 40;
 constexpr double EPS = 2.220446049250313e-16;
 
+constexpr int JW = 16;       // column block width
+constexpr int JC = 2 * JW;   // resident block pair = one warp's lanes
+constexpr int GP = JC + 1;   // odd pitch of the smem row-major tiles
+
 struct Args {
-  double* A;   // n x npad, ld
-  double* V;   // n x npad, ld
+  double* A;   // ne x npad, ld (rows >= n zero)
+  double* V;   // ne x npad, ld
   long ld;
-  int n, nblk;  // nblk = 2G blocks of W columns
+  int ne, nblk;  // padded rows (a multiple of 2 * cluster size); 2P blocks of JW columns
   double tol;
   int* rot;     // [MAX_SWEEPS] rotation counters (zeroed)
   int* status;  // sweeps used / -1
@@ -48,122 +75,395 @@ __device__ inline void round_pair(int N, int r, int k, int* p, int* q) {
   }
 }
 
-// Rotate columns x, y (length n, smem) so that they become orthogonal.
-// Returns true when a rotation was applied.  Executed by one full warp; the
-// three dot products share one interleaved shuffle tree.
-__device__ __forceinline__ bool rotate_pair(double* __restrict__ ax, double* __restrict__ ay,
-                                            double* __restrict__ vx, double* __restrict__ vy,
-                                            int n, double tol2) {
-  const int lane = threadIdx.x & 31;
-  double alpha = 0.0, beta = 0.0, gamma = 0.0;
-  for (int i = lane; i < n; i += 32) {
-    const double x = ax[i], y = ay[i];
-    alpha = fma(x, x, alpha);
-    beta = fma(y, y, beta);
-    gamma = fma(x, y, gamma);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    alpha += __shfl_xor_sync(0xffffffffu, alpha, o);
-    beta += __shfl_xor_sync(0xffffffffu, beta, o);
-    gamma += __shfl_xor_sync(0xffffffffu, gamma, o);
-  }
-  // |gamma| > tol * sqrt(alpha * beta), evaluated without square roots when
-  // the product is safely representable.
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+__device__ __forceinline__ double ld_dsmem(const double* p, unsigned rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(p)), "r"(rank));
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra) : "memory");
+  return v;
+}
+
+// Rotation of columns (x, y) that annihilates gamma = a_x^T a_y, from the
+// Gram entries (alpha = |a_x|^2, beta = |a_y|^2): a_x' = c a_x - s a_y,
+// a_y' = s a_x + c a_y, t = s / c the smaller root of t^2 + 2 zeta t - 1 = 0,
+// zeta = (beta - alpha) / (2 gamma), i.e. t = sign(d) g / (|d| + sqrt(d^2 + g^2))
+// with d = beta - alpha, g = 2 gamma.  Returns false when
+// |gamma| <= tol sqrt(alpha beta) (the convergence test, in fp64).
+//
+// The angle only steers convergence; orthogonality needs c^2 + s^2 = 1 to
+// fp64 precision.  So t is evaluated in fp32 on the exponent-normalised
+// (d, g) (relative error ~1e-7: the pair is left with |gamma'| ~ 1e-7
+// |gamma|, which later sweeps remove like any other off-diagonal mass), and
+// c = (1 + t^2)^(-1/2) is refined to fp64 by two Newton steps, s = c t
+// (fp64 division + sqrt + rsqrt cost ~570 cycles of dependent latency,
+// tools/lat_bench.cu).  Ratios beyond the fp32 range take the fp64 formula.
+__device__ __forceinline__ bool rotation(double alpha, double beta, double gamma, double tol2,
+                                         double* c, double* s) {
   const double ab = alpha * beta;
   bool rot;
   if (ab > 1e-280 && ab < 1e280) rot = gamma * gamma > tol2 * ab;
   else rot = fabs(gamma) > sqrt(tol2) * sqrt(alpha) * sqrt(beta);
   if (gamma == 0.0 || !rot) return false;
-  const double zeta = (beta - alpha) / (2.0 * gamma);
+  const double d = beta - alpha, g = 2.0 * gamma;
+  const double m = fmax(fabs(d), fabs(g));
+  const int e = (int)((__double_as_longlong(m) >> 52) & 0x7ff);  // biased exponent of m
   double t;
-  if (fabs(zeta) > 1e150)
-    t = 0.5 / zeta;
-  else
-    t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-  const double c = rsqrt(fma(t, t, 1.0));
-  const double s = c * t;
-  for (int i = lane; i < n; i += 32) {
-    const double x = ax[i], y = ay[i];
-    ax[i] = fma(c, x, -s * y);
-    ay[i] = fma(s, x, c * y);
-    const double u = vx[i], w = vy[i];
-    vx[i] = fma(c, u, -s * w);
-    vy[i] = fma(s, u, c * w);
+  bool done = false;
+  if (e > 0 && e < 2046) {
+    const double sc = __longlong_as_double((long long)(2046 - e) << 52);  // 2^(1023 - e), exact
+    const float df = (float)(d * sc), gf = (float)(g * sc);                 // max(|df|, |gf|) in [1, 2)
+    const float af = fabsf(df);
+    const float x = fmaf(df, df, gf * gf);
+    const float tf = __fdividef(gf, af + x * rsqrtf(x));
+    if (fabsf(tf) > 1e-30f) {
+      t = (d < 0.0) ? -(double)tf : (double)tf;
+      done = true;
+    }
   }
+  if (!done) {  // fp64 path (ratio |g / d| outside the fp32 range)
+    double dd = d, gg = g;
+    if (m > 1e150 || m < 1e-150) {
+      const int ex = ilogb(m);
+      dd = scalbn(dd, -ex);
+      gg = scalbn(gg, -ex);
+    }
+    t = (dd < 0.0 ? -gg : gg) / (fabs(dd) + sqrt(fma(dd, dd, gg * gg)));
+  }
+  const double x = fma(t, t, 1.0);
+  double r = (double)rsqrtf((float)x);
+  const double hx = 0.5 * x;
+  r = r * fma(-hx * r, r, 1.5);
+  r = r * fma(-hx * r, r, 1.5);
+  *c = r;
+  *s = r * t;
   return true;
 }
 
-// Persistent cooperative kernel: G CTAs, 2G blocks of W columns.  Every round
-// each CTA owns one block pair (circle-method tournament over blocks) and
-// rotates only the W^2 cross pairs (W sub-rounds of W disjoint pairs, one
-// warp per pair); the intra-block pairs are swept once per sweep in round 0.
-// Sequential sub-rounds per sweep: (W-1) + (2G-1) W  ~ n.
-template <int W>
-__global__ void __launch_bounds__(32 * W, 1) jacobi_rounds_kernel(Args a) {
+// Pair p (0..JW-1) of a sub-round.  Intra (round 0 of a sweep): circle method
+// inside each of the two blocks, JW/2 pairs each.  Cross step s: (p, JW + (p + s) mod JW).
+__device__ __forceinline__ void pair_of(bool cross, int step, int p, int* x, int* y) {
+  if (cross) {
+    *x = p;
+    *y = JW + ((p + step) % JW);
+  } else {
+    const int blk = p / (JW / 2), k = p % (JW / 2);
+    round_pair(JW, step, k, x, y);
+    *x += blk * JW;
+    *y += blk * JW;
+  }
+}
+
+// Sub-round schedule: NSUB = (JW - 1) intra + JW cross sub-rounds.  Per
+// sub-round u and index i (0..JC-1): pair id (bits 0-3), role y (bit 4),
+// partner index (bits 5-9); the pair list (x, y) per u.
+constexpr int NSUB = 2 * JW - 1;
+
+struct Sched {
+  unsigned short idx[NSUB][JC];
+  unsigned char px[NSUB][JW], py[NSUB][JW];
+};
+
+__device__ __forceinline__ void build_sched(Sched* sc) {
+  for (int t = threadIdx.x; t < NSUB * JW; t += blockDim.x) {
+    const int u = t / JW, p = t % JW;
+    int x, y;
+    pair_of(u >= JW - 1, u >= JW - 1 ? u - (JW - 1) : u, p, &x, &y);
+    sc->px[u][p] = (unsigned char)x;
+    sc->py[u][p] = (unsigned char)y;
+    sc->idx[u][x] = (unsigned short)(p | (y << 5));
+    sc->idx[u][y] = (unsigned short)(p | 16 | (x << 5));
+  }
+}
+
+// The 2 x 2 block update of Gn = Q^T G Q: rows (i, partner i2) x columns
+// (xq, yq) of G -> row i of the block of Gn.  rp / rq: rotations of the
+// row / column pairs (identity if not rotated), yi: i is the y of its pair,
+// zero: the block is the annihilated pair's own (that entry is set to 0).
+__device__ __forceinline__ void gram_rot2(double a0, double a1, double b0, double b1, double2 rp,
+                                          double2 rq, int yi, bool zero, double* g0, double* g1) {
+  // row i of R_p^T M (R = [c s; -s c]): x-row c m_x - s m_y, y-row s m_x + c m_y
+  double n0, n1;
+  if (yi) {
+    n0 = fma(rp.y, b0, rp.x * a0);
+    n1 = fma(rp.y, b1, rp.x * a1);
+  } else {
+    n0 = fma(rp.x, a0, -rp.y * b0);
+    n1 = fma(rp.x, a1, -rp.y * b1);
+  }
+  *g0 = fma(n0, rq.x, -n1 * rq.y);
+  *g1 = fma(n0, rq.y, n1 * rq.x);
+  if (zero) {
+    if (yi) *g0 = 0.0;
+    else *g1 = 0.0;
+  }
+}
+
+// Look-ahead table: for sub-round u >= 1 and pair p, the pair (x, y) of u
+// and, for x and y, their pair / role / partner in sub-round u - 1
+// (5 + 5 + 2 x 10 bits), so the rotation warp forms the three Gram entries
+// of every pair of u from G_{u-1} without dependent index loads.
+__device__ __forceinline__ void build_lookahead(const Sched* sc, unsigned* la) {
+  for (int t = threadIdx.x; t < NSUB * JW; t += blockDim.x) {
+    const int u = t / JW, pp = t % JW;
+    if (u == 0) continue;
+    const unsigned x = sc->px[u][pp], y = sc->py[u][pp];
+    const unsigned ix = sc->idx[u - 1][x] & 0x3ff, iy = sc->idx[u - 1][y] & 0x3ff;
+    la[t] = x | (y << 5) | (ix << 10) | (iy << 20);
+  }
+}
+
+// Gram entries (x, x), (y, y), (x, y) of G_u = Q^T G_{u-1} Q for the pair
+// packed in w (build_lookahead); same arithmetic as the update threads.
+__device__ __forceinline__ void gram_lookahead(unsigned w, const double* __restrict__ G, const double2* cs,
+                                               unsigned mask, double* al, double* be, double* ga) {
+  const int x = w & 31, y = (w >> 5) & 31;
+  const int px = (w >> 10) & 15, rx = (w >> 14) & 1, x2 = (w >> 15) & 31;
+  const int py = (w >> 20) & 15, ry = (w >> 24) & 1, y2 = (w >> 25) & 31;
+  // column pairs ordered (x-member, y-member) of sub-round u - 1
+  const int cx0 = rx ? x2 : x, cx1 = rx ? x : x2;
+  const int cy0 = ry ? y2 : y, cy1 = ry ? y : y2;
+  const double xx0 = G[x * GP + cx0], xx1 = G[x * GP + cx1], xx2 = G[x2 * GP + cx0], xx3 = G[x2 * GP + cx1];
+  const double yy0 = G[y * GP + cy0], yy1 = G[y * GP + cy1], yy2 = G[y2 * GP + cy0], yy3 = G[y2 * GP + cy1];
+  const double xy0 = G[x * GP + cy0], xy1 = G[x * GP + cy1], xy2 = G[x2 * GP + cy0], xy3 = G[x2 * GP + cy1];
+  const double2 rpx = cs[px], rpy = cs[py];
+  const bool mx = (mask >> px) & 1, my = (mask >> py) & 1;
+  double g0, g1;
+  gram_rot2(xx0, xx1, xx2, xx3, rpx, rpx, rx, mx, &g0, &g1);
+  *al = rx ? g1 : g0;
+  gram_rot2(yy0, yy1, yy2, yy3, rpy, rpy, ry, my, &g0, &g1);
+  *be = ry ? g1 : g0;
+  gram_rot2(xy0, xy1, xy2, xy3, rpx, rpy, rx, mx && px == py, &g0, &g1);
+  *ga = ry ? g1 : g0;
+}
+
+// Block one-sided Jacobi, Gram formulation.  2P blocks of JW columns; every
+// round of the circle-method tournament pairs them up; pair p is owned by one
+// thread-block cluster of C CTAs, CTA r holding rows [r R, (r+1) R) of the
+// pair's 2 JW columns of A and V in shared memory (R = ne / C).  Per round:
+//   1. partial Gram G_r = A_r^T A_r (JC x JC) of the slice;
+//   2. G = sum_r G_r read over DSMEM in rank order (every CTA of the cluster
+//      forms the same G bitwise);
+//   3. the JW - 1 intra-block sub-rounds (round 0 of a sweep) and JW cross
+//      sub-rounds run on G (JC x JC), accumulating the rotations into J;
+//   4. A_r <- A_r J, V_r <- V_r J; store; grid barrier.
+// The rotations, their order and the convergence test are those of the
+// classic column-pair sweep; only the column updates are batched per round
+// (one small GEMM instead of ~JW rotations of every column), and the rows are
+// split over C SMs.
+//
+// Sub-rounds are software-pipelined over one block barrier each: warps
+// 0..JW-1 apply sub-round k (Gn = Q_k^T G Q_k, J <- J Q_k) while the extra
+// rotation warp JW forms, from the same G and Q_k, the three Gram entries of
+// every pair of sub-round k+1 and computes Q_{k+1}.
+constexpr int JTHREADS = 32 * (JW + 1);
+
+__global__ void __launch_bounds__(JTHREADS, 1) jacobi_rounds_kernel(Args a) {
   extern __shared__ double sm[];
-  const int n = a.n;
-  const int ldS = n;
-  double* As = sm;                        // 2W columns
-  double* Vs = sm + (size_t)2 * W * ldS;  // 2W columns
-  __shared__ int s_rot;
-  const int G = gridDim.x, g = blockIdx.x;
+  unsigned C, r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(C));
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  const int p = blockIdx.x / C;
+  const int R = a.ne / C;
+  const long row0 = (long)r * R;
+  double* As = sm;                  // R x JC row-major, pitch GP
+  double* Vs = As + (size_t)R * GP;
+  double* Gp = Vs + (size_t)R * GP;  // JC x JC partial (dense, pitch JC)
+  double* G = Gp + JC * JC;          // JC x GP, two buffers
+  double* J = G + 2 * JC * GP;       // JC x GP
+  __shared__ unsigned s_mask[2];
+  __shared__ double2 CS[2][JW];
+  __shared__ Sched sc;
+  __shared__ unsigned la[NSUB * JW];
+  build_sched(&sc);
+  __syncthreads();
+  build_lookahead(&sc, la);
   const int N = a.nblk;
-  const int warp = threadIdx.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool rwarp = warp == JW;  // the rotation warp
   const double tol2 = a.tol * a.tol;
   unsigned bar = 0;
   int sweep = 0;
+#ifdef JAC_PROBE
+  unsigned long long probe_last = gtime();
+  const long long clk0 = clock64();
+  long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
   for (; sweep < MAX_SWEEPS; ++sweep) {
-    for (int r = 0; r < N - 1; ++r) {
+    for (int rr = 0; rr < N - 1; ++rr) {
       int bp, bq;
-      round_pair(N, r, g, &bp, &bq);
-      // load the two blocks (16-byte vector loads; n is padded to even)
-      const int n2 = n >> 1;
-      for (int idx = threadIdx.x; idx < 2 * W * n2; idx += 32 * W) {
-        const int c = idx / n2, i = (idx - c * n2) * 2;
-        const int gc = (c < W ? bp * W + c : bq * W + (c - W));
-        const double2 va = __ldcg((const double2*)&a.A[i + (long)gc * a.ld]);
-        const double2 vv = __ldcg((const double2*)&a.V[i + (long)gc * a.ld]);
-        *(double2*)&As[c * ldS + i] = va;
-        *(double2*)&Vs[c * ldS + i] = vv;
+      round_pair(N, rr, p, &bp, &bq);
+      // 1. load the slice (16-byte global loads along the columns)
+      const int R2 = R >> 1;
+      for (int idx = threadIdx.x; idx < JC * R2; idx += JTHREADS) {
+        const int col = idx / R2, i = (idx - col * R2) * 2;
+        const int gc = col < JW ? bp * JW + col : bq * JW + (col - JW);
+        const long off = row0 + i + (long)gc * a.ld;
+        const double2 va = __ldcg((const double2*)&a.A[off]);
+        const double2 vv = __ldcg((const double2*)&a.V[off]);
+        As[i * GP + col] = va.x;
+        As[(i + 1) * GP + col] = va.y;
+        Vs[i * GP + col] = vv.x;
+        Vs[(i + 1) * GP + col] = vv.y;
       }
-      if (threadIdx.x == 0) s_rot = 0;
+      for (int idx = threadIdx.x; idx < JC * JC; idx += JTHREADS) {
+        const int i = idx / JC, j = idx - i * JC;
+        J[i * GP + j] = (i == j) ? 1.0 : 0.0;
+      }
+      __syncthreads();
+      JPROBE(0);
+      // 2. partial Gram: warp w rows w and w + JW, lane j column j
+      if (!rwarp) {
+        double g0 = 0.0, g1 = 0.0, h0 = 0.0, h1 = 0.0;
+        int k = 0;
+        for (; k + 1 < R; k += 2) {
+          const double v = As[k * GP + lane], w = As[(k + 1) * GP + lane];
+          g0 = fma(As[k * GP + warp], v, g0);
+          g1 = fma(As[k * GP + warp + JW], v, g1);
+          h0 = fma(As[(k + 1) * GP + warp], w, h0);
+          h1 = fma(As[(k + 1) * GP + warp + JW], w, h1);
+        }
+        Gp[warp * JC + lane] = g0 + h0;
+        Gp[(warp + JW) * JC + lane] = g1 + h1;
+      }
+      JPROBE(1);
+      if (C > 1) cluster_sync_all();
+      else __syncthreads();
+      for (int idx = threadIdx.x; idx < JC * JC; idx += JTHREADS) {
+        double part[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < (int)C) part[q] = (q == (int)r) ? Gp[idx] : ld_dsmem(&Gp[idx], q);
+        double g = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < (int)C) g += part[q];
+        G[(idx / JC) * GP + (idx % JC)] = g;
+      }
+      __syncthreads();
+      JPROBE(2);
+      // 3. sub-rounds on G (ping-pong buffers), pipelined
+      const int u0 = rr == 0 ? 0 : JW - 1;  // first schedule index of this round
+      const int K = NSUB - u0;
+      if (rwarp) {  // rotations of the first sub-round, from G directly
+        const int pl = lane & (JW - 1);
+        const int x = sc.px[u0][pl], y = sc.py[u0][pl];
+        double c = 1.0, sn = 0.0;
+        const bool rot = rotation(G[x * GP + x], G[y * GP + y], G[x * GP + y], tol2, &c, &sn);
+        const unsigned mask = __ballot_sync(0xffffffffu, rot) & ((1u << JW) - 1);
+        if (lane < JW) CS[0][lane] = make_double2(c, sn);
+        if (lane == 0) s_mask[0] = mask;
+      }
       __syncthreads();
       int nrot = 0;
-      if (r == 0) {
-        // intra-block pairs of both resident blocks: round robin on W columns
-        for (int sr = 0; sr < W - 1; ++sr) {
-          const int blk = warp / (W / 2), k = warp % (W / 2);
-          int x, y;
-          round_pair(W, sr, k, &x, &y);
-          x += blk * W;
-          y += blk * W;
-          nrot += rotate_pair(As + x * ldS, As + y * ldS, Vs + x * ldS, Vs + y * ldS, n, tol2);
-          __syncthreads();
+      const double* gc = G;
+      double* gn = G + JC * GP;
+      for (int k = 0; k < K; ++k) {
+#ifdef JAC_PROBE
+        const long long c0 = clock64();
+#endif
+        const int u = u0 + k;
+        const double2* cs = CS[k & 1];
+        const unsigned mask = s_mask[k & 1];
+        nrot += __popc(mask);
+        if (!rwarp) {
+          const int i = threadIdx.x / JW, q = threadIdx.x % JW;
+          const int xq = sc.px[u][q], yq = sc.py[u][q];
+          const double jx = J[i * GP + xq], jy = J[i * GP + yq];
+          const unsigned si = sc.idx[u][i];
+          const int pi = si & 15, yi = (si >> 4) & 1, i2 = si >> 5;
+          double g0, g1;
+          gram_rot2(gc[i * GP + xq], gc[i * GP + yq], gc[i2 * GP + xq], gc[i2 * GP + yq], cs[pi], cs[q], yi,
+                    pi == q && ((mask >> q) & 1), &g0, &g1);
+          gn[i * GP + xq] = g0;
+          gn[i * GP + yq] = g1;
+          if ((mask >> q) & 1) {
+            const double2 rq = cs[q];
+            J[i * GP + xq] = fma(rq.x, jx, -rq.y * jy);
+            J[i * GP + yq] = fma(rq.y, jx, rq.x * jy);
+          }
+        } else if (k + 1 < K) {
+          double al, be, ga;
+          gram_lookahead(la[(u + 1) * JW + (lane & (JW - 1))], gc, cs, mask, &al, &be, &ga);
+#ifdef JAC_PROBE
+          long long cm;
+          asm volatile("mov.u64 %0, %%clock64;" : "=l"(cm) : "d"(al), "d"(be), "d"(ga) : "memory");
+#endif
+          double c = 1.0, sn = 0.0;
+          const bool rot = rotation(al, be, ga, tol2, &c, &sn);
+#ifdef JAC_PROBE
+          long long cr;
+          asm volatile("mov.u64 %0, %%clock64;" : "=l"(cr) : "d"(c), "d"(sn) : "memory");
+          pacc[6] += cm - c0;
+          pacc[7] += cr - cm;
+#endif
+          const unsigned m2 = __ballot_sync(0xffffffffu, rot) & ((1u << JW) - 1);
+          if (lane < JW) CS[(k + 1) & 1][lane] = make_double2(c, sn);
+          if (lane == 0) s_mask[(k + 1) & 1] = m2;
         }
-      }
-      // cross pairs (i, W + (i + s) mod W)
-      for (int s = 0; s < W; ++s) {
-        const int x = warp, y = W + ((warp + s) % W);
-        nrot += rotate_pair(As + x * ldS, As + y * ldS, Vs + x * ldS, Vs + y * ldS, n, tol2);
+#ifdef JAC_PROBE
+        const long long c1 = clock64();
+#endif
         __syncthreads();
+#ifdef JAC_PROBE
+        {
+          const int o = threadIdx.x == 0 ? 0 : 3;
+          pacc[o] += c1 - c0;
+          pacc[o + 1] += clock64() - c1;
+          pacc[o + 2] += 1;
+        }
+#endif
+        const double* t = gc;
+        gc = gn;
+        gn = const_cast<double*>(t);
       }
-      if ((threadIdx.x & 31) == 0 && nrot) atomicAdd(&s_rot, nrot);
-      __syncthreads();
-      if (threadIdx.x == 0 && s_rot) atomicAdd(&a.rot[sweep], s_rot);
-      for (int idx = threadIdx.x; idx < 2 * W * n2; idx += 32 * W) {
-        const int c = idx / n2, i = (idx - c * n2) * 2;
-        const int gc = (c < W ? bp * W + c : bq * W + (c - W));
-        *(double2*)&a.A[i + (long)gc * a.ld] = *(const double2*)&As[c * ldS + i];
-        *(double2*)&a.V[i + (long)gc * a.ld] = *(const double2*)&Vs[c * ldS + i];
+      JPROBE(3);
+      // 4. A_r <- A_r J, V_r <- V_r J (warp w rows w, w + JW, ...), store
+      if (nrot) {
+        if (!rwarp)
+          for (int k = warp; k < R; k += JW) {
+            double oa = 0.0, ov = 0.0;
+#pragma unroll 8
+            for (int l = 0; l < JC; ++l) {
+              const double jl = J[l * GP + lane];
+              oa = fma(As[k * GP + l], jl, oa);
+              ov = fma(Vs[k * GP + l], jl, ov);
+            }
+            __syncwarp();
+            As[k * GP + lane] = oa;
+            Vs[k * GP + lane] = ov;
+          }
+        __syncthreads();
+        JPROBE(4);
+        for (int idx = threadIdx.x; idx < JC * R2; idx += JTHREADS) {
+          const int col = idx / R2, i = (idx - col * R2) * 2;
+          const int gc2 = col < JW ? bp * JW + col : bq * JW + (col - JW);
+          const long off = row0 + i + (long)gc2 * a.ld;
+          *(double2*)&a.A[off] = make_double2(As[i * GP + col], As[(i + 1) * GP + col]);
+          *(double2*)&a.V[off] = make_double2(Vs[i * GP + col], Vs[(i + 1) * GP + col]);
+        }
+        if (r == 0 && threadIdx.x == 0) atomicAdd(&a.rot[sweep], nrot);
       }
+      JPROBE(5);
       ++bar;
-      if (G > 1) grid_barrier(a.ctr, bar * G);
-      else __syncthreads();
+      grid_barrier(a.ctr, bar * gridDim.x);
+      JPROBE(6);
     }
     if (__ldcg(&a.rot[sweep]) == 0) break;
   }
-  if (g == 0 && threadIdx.x == 0) *a.status = (sweep < MAX_SWEEPS) ? sweep + 1 : -1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *a.status = (sweep < MAX_SWEEPS) ? sweep + 1 : -1;
+#ifdef JAC_PROBE
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_probe[7] += clock64() - clk0;
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    for (int o = 0; o < 3; ++o) g_probe2[o] += pacc[o];
+  if (blockIdx.x == 0 && threadIdx.x == 32 * JW)
+    for (int o = 3; o < 8; ++o) g_probe2[o] += pacc[o];
+#endif
+  if (C > 1) cluster_sync_all();  // no CTA leaves while its Gp may still be read
 }
 
 __device__ inline double block_reduce_sum(double v, double* sh) {
@@ -293,32 +593,33 @@ __global__ void __launch_bounds__(1024) jacobi_finish_kernel(const double* __res
 }
 }  // namespace jac
 
-// Column-block width: the resident block pair (A and V, 2W columns each) must
-// fit the 200 KB smem budget: 4 W n 8 bytes.
-static inline int jac_width(int n) {
-  const int ne = n + (n & 1);
-  static const int forced = [] {  // tuning knob: UTV_JAC_W = 4 / 8 / 16
-    const char* e = getenv("UTV_JAC_W");
-    return e ? atoi(e) : 0;
-  }();
-  if ((forced == 4 || forced == 8 || forced == 16) && (size_t)4 * forced * ne * 8 <= 200 * 1024)
-    return forced;
-  if ((size_t)4 * 16 * ne * 8 <= 200 * 1024) return 16;
-  if ((size_t)4 * 8 * ne * 8 <= 200 * 1024) return 8;
-  return 4;
-}
-
-static inline int jac_blocks(int n, int W) {
-  int nb = (n + W - 1) / W;
+// Cluster size C (CTAs per block pair, each holding ne / C rows of the pair
+// in shared memory).  Rows per CTA stay <= 256 (smem), CTAs <= 148 (the
+// cooperative grid must be co-resident).  Tuning knob UTV_JAC_CLUSTER.
+static inline int jac_blocks(int n) {
+  int nb = (n + jac::JW - 1) / jac::JW;
   if (nb & 1) nb++;
   if (nb < 2) nb = 2;
   return nb;
 }
 
+static inline int jac_cluster(int n) {
+  static const int forced = [] {
+    const char* e = getenv("UTV_JAC_CLUSTER");
+    return e ? atoi(e) : 0;
+  }();
+  const int pairs = jac_blocks(n) / 2;
+  int c = forced == 1 || forced == 2 || forced == 4 || forced == 8 ? forced : (n >= 128 ? 4 : (n >= 32 ? 2 : 1));
+  while (c > 1 && pairs * c > 148) c >>= 1;
+  while (c < 8 && (round_up(n, 2 * c) / c) > 256) c <<= 1;
+  return c;
+}
+
+static inline long jac_ld(int n) { return round_up(n, 16); }
+
 size_t gesvj_ws_doubles(int n) {
-  const long ld = round_up(n, 4);
-  const int W = jac_width(n);
-  const long npad = (long)jac_blocks(n, W) * W;
+  const long ld = jac_ld(n);
+  const long npad = (long)jac_blocks(n) * jac::JW;
   return 2 * ld * npad + 2048 + (size_t)jac::MAX_SWEEPS + 64 + 4 * 32;
 }
 
@@ -335,18 +636,19 @@ int gesvj_ex(Mat A, double* sigma, Mat U, Mat V, double* ws, size_t ws_doubles, 
   const int n = A.rows;
   if (n <= 0) return UTV_OK;
   if (n > 1024) return -1;
-  const long ld = round_up(n, 4);
-  const int W = jac_width(n);
-  const int nblk = jac_blocks(n, W);
-  const long npad = (long)nblk * W;
+  const long ld = jac_ld(n);
+  const int nblk = jac_blocks(n);
+  const long npad = (long)nblk * jac::JW;
+  const int C = jac_cluster(n);
   Arena ar{(char*)ws, ws_doubles * sizeof(double), 0};
   double* Aw = ar.take(ld * npad);
   double* Vw = ar.take(ld * npad);
   double* ctl = ar.take(jac::MAX_SWEEPS + 64);
   double* scratch = ar.take(1024);
   if (!scratch) return UTV_ERR_WORKSPACE;
-  // rows are padded to an even count (16-byte vector moves); padding is zero
-  const int ne = n + (n & 1);
+  // rows are padded to a multiple of 2C (16-byte vector moves, equal slices);
+  // padding is zero
+  const int ne = (int)round_up(n, 2 * C);
   // The rounds run on A^T (UTV_JAC_TRANSPOSE, default on): for the graded
   // upper-triangular blocks randUTV hands in, the columns of R^T start much
   // closer to orthogonal, so far fewer rotations fire (256^2 Gaussian-decay
@@ -366,31 +668,38 @@ int gesvj_ex(Mat A, double* sigma, Mat U, Mat V, double* ws, size_t ws_doubles, 
   UTV_CUDA(cudaMemsetAsync(ctl, 0, (jac::MAX_SWEEPS + 64) * sizeof(double), st));
   jac::Args a;
   a.A = Aw; a.V = Vw; a.ld = ld;
-  a.n = ne; a.nblk = nblk;
+  a.ne = ne; a.nblk = nblk;
   a.tol = 4.0 * sqrt((double)n) * jac::EPS;
   a.rot = (int*)ctl;
   a.ctr = (unsigned*)(ctl + jac::MAX_SWEEPS);
   a.status = status_dev;
-  const int G = nblk / 2;
-  const size_t smem = (size_t)4 * W * ne * sizeof(double);
+  const int R = ne / C;
+  const size_t smem = ((size_t)2 * R * jac::GP + jac::JC * jac::JC + 3 * jac::JC * jac::GP) * sizeof(double);
   if (!g_jac_attr) {
-    for (auto f : {jac::jacobi_rounds_kernel<16>, jac::jacobi_rounds_kernel<8>, jac::jacobi_rounds_kernel<4>})
-      UTV_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    UTV_CUDA(cudaFuncSetAttribute(jac::jacobi_rounds_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     UTV_CUDA(cudaFuncSetAttribute(jac::jacobi_finish_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     g_jac_attr = true;
   }
   if (smem > 200 * 1024) return -1;
   {
-  ProfScope ps(PROF_JACOBI, 0.0, 0.0, st);
-  void* kfn = W == 16 ? (void*)jac::jacobi_rounds_kernel<16>
-              : (W == 8 ? (void*)jac::jacobi_rounds_kernel<8> : (void*)jac::jacobi_rounds_kernel<4>);
-  void* args[] = {&a};
-  if (G > 1) {
-    UTV_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(G), dim3(32 * W), args, smem, st));
-  } else {
-    UTV_CUDA(cudaLaunchKernel(kfn, dim3(1), dim3(32 * W), args, smem, st));
-  }
+    ProfScope ps(PROF_JACOBI, 0.0, 0.0, st);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((nblk / 2) * C);
+    cfg.blockDim = dim3(jac::JTHREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    UTV_CUDA(cudaLaunchKernelEx(&cfg, jac::jacobi_rounds_kernel, a));
   }
   const size_t smem2 = (size_t)4 * (n + 2) * sizeof(double);
   ProfScope ps2(PROF_JFINISH, 0.0, 0.0, st);

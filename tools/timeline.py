@@ -60,3 +60,22 @@ for st, v in per_stream.items(): print(f"  stream {st}: {v:.2f} ms of launches")
 psc = collections.defaultdict(float)
 for s_, e_, c_, st_ in ev: psc[(st_, names[c_])] += e_ - s_
 for (st_, c_), v in sorted(psc.items()): print(f"    {st_} {c_:14s} {v:9.2f} ms")
+# critical-path stalls of the main stream: idle gaps of the stream "(nil)"
+# that end within 50 us of a side-stream kernel's end (the main stream was
+# waiting on that event)
+main = sorted((s, e, names[c]) for s, e, c, st in ev if st == "(nil)")
+side = sorted((e, names[c], st) for s, e, c, st in ev if st != "(nil)")
+stall = collections.defaultdict(float)
+gaps, cnt = 0.0, collections.Counter()
+for (s0, e0, _), (s1, e1, _) in zip(main, main[1:]):
+    g = s1 - e0
+    if g <= 0.005:
+        continue
+    gaps += g
+    last = [x for x in side if e0 - 1e-3 <= x[0] <= s1 + 1e-3]
+    key = last[-1][1] if last else "none"
+    stall[key] += g
+    cnt[key] += 1
+print(f"  main-stream idle gaps > 5 us: {gaps:.2f} ms")
+for k, v in sorted(stall.items(), key=lambda kv: -kv[1]):
+    print(f"    ended by {k:14s} {v:9.2f} ms over {cnt[k]} gaps")
