@@ -91,17 +91,15 @@ __device__ __forceinline__ double ld_dsmem(const double* p, unsigned rank) {
 // Rotation of columns (x, y) that annihilates gamma = a_x^T a_y, from the
 // Gram entries (alpha = |a_x|^2, beta = |a_y|^2): a_x' = c a_x - s a_y,
 // a_y' = s a_x + c a_y, t = s / c the smaller root of t^2 + 2 zeta t - 1 = 0,
-// zeta = (beta - alpha) / (2 gamma), i.e. t = sign(d) g / (|d| + sqrt(d^2 + g^2))
-// with d = beta - alpha, g = 2 gamma.  Returns false when
-// |gamma| <= tol sqrt(alpha beta) (the convergence test, in fp64).
-//
-// The angle only steers convergence; orthogonality needs c^2 + s^2 = 1 to
-// fp64 precision.  So t is evaluated in fp32 on the exponent-normalised
-// (d, g) (relative error ~1e-7: the pair is left with |gamma'| ~ 1e-7
-// |gamma|, which later sweeps remove like any other off-diagonal mass), and
-// c = (1 + t^2)^(-1/2) is refined to fp64 by two Newton steps, s = c t
-// (fp64 division + sqrt + rsqrt cost ~570 cycles of dependent latency,
-// tools/lat_bench.cu).  Ratios beyond the fp32 range take the fp64 formula.
+// zeta = (beta - alpha) / (2 gamma).  Returns false when
+// |gamma| <= tol sqrt(alpha beta) (the convergence test).  With
+// d = beta - alpha, g = 2 gamma, h = sqrt(d^2 + g^2):
+//   c = (h + |d|) / sqrt(2 h (h + |d|)),  s = sign(d) g / sqrt(2 h (h + |d|))
+// (c^2 + s^2 = 1, no cancellation) — one sqrt and one rsqrt on the
+// dependent chain: 294 cycles against 513 for the zeta form with its two
+// divisions (tools/rot_bench.cu); the rotation is the critical path of
+// every sub-round.  (d, g) are rescaled exactly by a power of two when out
+// of the safe range.
 __device__ __forceinline__ bool rotation(double alpha, double beta, double gamma, double tol2,
                                          double* c, double* s) {
   const double ab = alpha * beta;
@@ -109,38 +107,19 @@ __device__ __forceinline__ bool rotation(double alpha, double beta, double gamma
   if (ab > 1e-280 && ab < 1e280) rot = gamma * gamma > tol2 * ab;
   else rot = fabs(gamma) > sqrt(tol2) * sqrt(alpha) * sqrt(beta);
   if (gamma == 0.0 || !rot) return false;
-  const double d = beta - alpha, g = 2.0 * gamma;
+  double d = beta - alpha, g = 2.0 * gamma;
   const double m = fmax(fabs(d), fabs(g));
-  const int e = (int)((__double_as_longlong(m) >> 52) & 0x7ff);  // biased exponent of m
-  double t;
-  bool done = false;
-  if (e > 0 && e < 2046) {
+  if (m > 1e150 || m < 1e-150) {
+    const int e = (int)((__double_as_longlong(m) >> 52) & 0x7ff);  // biased exponent, m normal
     const double sc = __longlong_as_double((long long)(2046 - e) << 52);  // 2^(1023 - e), exact
-    const float df = (float)(d * sc), gf = (float)(g * sc);                 // max(|df|, |gf|) in [1, 2)
-    const float af = fabsf(df);
-    const float x = fmaf(df, df, gf * gf);
-    const float tf = __fdividef(gf, af + x * rsqrtf(x));
-    if (fabsf(tf) > 1e-30f) {
-      t = (d < 0.0) ? -(double)tf : (double)tf;
-      done = true;
-    }
+    d *= sc;
+    g *= sc;
   }
-  if (!done) {  // fp64 path (ratio |g / d| outside the fp32 range)
-    double dd = d, gg = g;
-    if (m > 1e150 || m < 1e-150) {
-      const int ex = ilogb(m);
-      dd = scalbn(dd, -ex);
-      gg = scalbn(gg, -ex);
-    }
-    t = (dd < 0.0 ? -gg : gg) / (fabs(dd) + sqrt(fma(dd, dd, gg * gg)));
-  }
-  const double x = fma(t, t, 1.0);
-  double r = (double)rsqrtf((float)x);
-  const double hx = 0.5 * x;
-  r = r * fma(-hx * r, r, 1.5);
-  r = r * fma(-hx * r, r, 1.5);
-  *c = r;
-  *s = r * t;
+  const double h = sqrt(fma(d, d, g * g));
+  const double u = h + fabs(d);
+  const double q = rsqrt(2.0 * h * u);
+  *c = u * q;
+  *s = (d < 0.0 ? -g : g) * q;
   return true;
 }
 
@@ -217,28 +196,49 @@ __device__ __forceinline__ void build_lookahead(const Sched* sc, unsigned* la) {
   }
 }
 
-// Gram entries (x, x), (y, y), (x, y) of G_u = Q^T G_{u-1} Q for the pair
-// packed in w (build_lookahead); same arithmetic as the update threads.
-__device__ __forceinline__ void gram_lookahead(unsigned w, const double* __restrict__ G, const double2* cs,
-                                               unsigned mask, double* al, double* be, double* ga) {
+// Diagonal of the rotated 2 x 2 pair block [[al, ga], [ga, be]] (the
+// update threads' arithmetic for those entries, G symmetric).
+__device__ __forceinline__ void pair_diag(double al, double be, double ga, double2 r, bool rot, double* dx,
+                                          double* dy) {
+  if (!rot) {
+    *dx = al;
+    *dy = be;
+    return;
+  }
+  double g0, g1, h0, h1;
+  gram_rot2(al, ga, ga, be, r, r, 0, true, &g0, &g1);
+  gram_rot2(ga, be, al, ga, r, r, 1, true, &h0, &h1);
+  *dx = g0;
+  *dy = h1;
+}
+
+// Rotation warp, lane p: rotation of pair p of sub-round u + 1 from
+// G_u = Q_u^T G_{u-1} Q_u.  The diagonal entries come from the lanes that
+// rotated them in sub-round u (their registers dX, dY; shuffles), so only
+// the off-diagonal gamma is formed from G_{u-1} (4 loads).  Updates
+// (cK, sK, rK, dX, dY) to sub-round u + 1.
+__device__ __forceinline__ void rotate_next(unsigned w, const double* __restrict__ G, double tol2,
+                                            double* cK, double* sK, bool* rK, double* dX, double* dY) {
   const int x = w & 31, y = (w >> 5) & 31;
   const int px = (w >> 10) & 15, rx = (w >> 14) & 1, x2 = (w >> 15) & 31;
   const int py = (w >> 20) & 15, ry = (w >> 24) & 1, y2 = (w >> 25) & 31;
-  // column pairs ordered (x-member, y-member) of sub-round u - 1
-  const int cx0 = rx ? x2 : x, cx1 = rx ? x : x2;
   const int cy0 = ry ? y2 : y, cy1 = ry ? y : y2;
-  const double xx0 = G[x * GP + cx0], xx1 = G[x * GP + cx1], xx2 = G[x2 * GP + cx0], xx3 = G[x2 * GP + cx1];
-  const double yy0 = G[y * GP + cy0], yy1 = G[y * GP + cy1], yy2 = G[y2 * GP + cy0], yy3 = G[y2 * GP + cy1];
-  const double xy0 = G[x * GP + cy0], xy1 = G[x * GP + cy1], xy2 = G[x2 * GP + cy0], xy3 = G[x2 * GP + cy1];
-  const double2 rpx = cs[px], rpy = cs[py];
-  const bool mx = (mask >> px) & 1, my = (mask >> py) & 1;
+  const double m0 = G[x * GP + cy0], m1 = G[x * GP + cy1], m2 = G[x2 * GP + cy0], m3 = G[x2 * GP + cy1];
+  const unsigned full = 0xffffffffu;
+  const double ax = __shfl_sync(full, *dX, px), ay = __shfl_sync(full, *dY, px);
+  const double bx = __shfl_sync(full, *dX, py), by = __shfl_sync(full, *dY, py);
+  const double2 rpx = make_double2(__shfl_sync(full, *cK, px), __shfl_sync(full, *sK, px));
+  const double2 rpy = make_double2(__shfl_sync(full, *cK, py), __shfl_sync(full, *sK, py));
+  const double al = rx ? ay : ax, be = ry ? by : bx;
   double g0, g1;
-  gram_rot2(xx0, xx1, xx2, xx3, rpx, rpx, rx, mx, &g0, &g1);
-  *al = rx ? g1 : g0;
-  gram_rot2(yy0, yy1, yy2, yy3, rpy, rpy, ry, my, &g0, &g1);
-  *be = ry ? g1 : g0;
-  gram_rot2(xy0, xy1, xy2, xy3, rpx, rpy, rx, mx && px == py, &g0, &g1);
-  *ga = ry ? g1 : g0;
+  gram_rot2(m0, m1, m2, m3, rpx, rpy, rx, false, &g0, &g1);
+  const double ga = ry ? g1 : g0;
+  double c = 1.0, sn = 0.0;
+  const bool rot = rotation(al, be, ga, tol2, &c, &sn);
+  *cK = c;
+  *sK = sn;
+  *rK = rot;
+  pair_diag(al, be, ga, make_double2(c, sn), rot, dX, dY);
 }
 
 // Block one-sided Jacobi, Gram formulation.  2P blocks of JW columns; every
@@ -349,13 +349,16 @@ __global__ void __launch_bounds__(JTHREADS, 1) jacobi_rounds_kernel(Args a) {
       // 3. sub-rounds on G (ping-pong buffers), pipelined
       const int u0 = rr == 0 ? 0 : JW - 1;  // first schedule index of this round
       const int K = NSUB - u0;
+      double cK = 1.0, sK = 0.0, dX = 0.0, dY = 0.0;  // rotation warp state (own pair)
+      bool rK = false;
       if (rwarp) {  // rotations of the first sub-round, from G directly
         const int pl = lane & (JW - 1);
         const int x = sc.px[u0][pl], y = sc.py[u0][pl];
-        double c = 1.0, sn = 0.0;
-        const bool rot = rotation(G[x * GP + x], G[y * GP + y], G[x * GP + y], tol2, &c, &sn);
-        const unsigned mask = __ballot_sync(0xffffffffu, rot) & ((1u << JW) - 1);
-        if (lane < JW) CS[0][lane] = make_double2(c, sn);
+        const double al = G[x * GP + x], be = G[y * GP + y], ga = G[x * GP + y];
+        rK = rotation(al, be, ga, tol2, &cK, &sK);
+        pair_diag(al, be, ga, make_double2(cK, sK), rK, &dX, &dY);
+        const unsigned mask = __ballot_sync(0xffffffffu, rK) & ((1u << JW) - 1);
+        if (lane < JW) CS[0][lane] = make_double2(cK, sK);
         if (lane == 0) s_mask[0] = mask;
       }
       __syncthreads();
@@ -370,39 +373,39 @@ __global__ void __launch_bounds__(JTHREADS, 1) jacobi_rounds_kernel(Args a) {
         const double2* cs = CS[k & 1];
         const unsigned mask = s_mask[k & 1];
         nrot += __popc(mask);
-        if (!rwarp) {
-          const int i = threadIdx.x / JW, q = threadIdx.x % JW;
-          const int xq = sc.px[u][q], yq = sc.py[u][q];
-          const double jx = J[i * GP + xq], jy = J[i * GP + yq];
-          const unsigned si = sc.idx[u][i];
-          const int pi = si & 15, yi = (si >> 4) & 1, i2 = si >> 5;
-          double g0, g1;
-          gram_rot2(gc[i * GP + xq], gc[i * GP + yq], gc[i2 * GP + xq], gc[i2 * GP + yq], cs[pi], cs[q], yi,
-                    pi == q && ((mask >> q) & 1), &g0, &g1);
-          gn[i * GP + xq] = g0;
-          gn[i * GP + yq] = g1;
+        if (threadIdx.x < JW * JW) {
+          // 2 x 2 block (row pair pb, column pair q) of Gn: both rows
+          const int pb = threadIdx.x / JW, q = threadIdx.x % JW;
+          const int xp = sc.px[u][pb], yp = sc.py[u][pb], xq = sc.px[u][q], yq = sc.py[u][q];
+          const double m00 = gc[xp * GP + xq], m01 = gc[xp * GP + yq];
+          const double m10 = gc[yp * GP + xq], m11 = gc[yp * GP + yq];
+          const double2 rp = cs[pb], rq = cs[q];
+          const bool z = pb == q && ((mask >> q) & 1);
+          double g0, g1, h0, h1;
+          gram_rot2(m00, m01, m10, m11, rp, rq, 0, z, &g0, &g1);
+          gram_rot2(m10, m11, m00, m01, rp, rq, 1, z, &h0, &h1);
+          gn[xp * GP + xq] = g0;
+          gn[xp * GP + yq] = g1;
+          gn[yp * GP + xq] = h0;
+          gn[yp * GP + yq] = h1;
+        } else if (!rwarp) {
+          // J <- J Q: rows k and k + JW of column pair q
+          const int tt = threadIdx.x - JW * JW, q = tt % JW, k0 = tt / JW;
           if ((mask >> q) & 1) {
+            const int xq = sc.px[u][q], yq = sc.py[u][q];
             const double2 rq = cs[q];
-            J[i * GP + xq] = fma(rq.x, jx, -rq.y * jy);
-            J[i * GP + yq] = fma(rq.y, jx, rq.x * jy);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int kk = k0 + h * JW;
+              const double jx = J[kk * GP + xq], jy = J[kk * GP + yq];
+              J[kk * GP + xq] = fma(rq.x, jx, -rq.y * jy);
+              J[kk * GP + yq] = fma(rq.y, jx, rq.x * jy);
+            }
           }
         } else if (k + 1 < K) {
-          double al, be, ga;
-          gram_lookahead(la[(u + 1) * JW + (lane & (JW - 1))], gc, cs, mask, &al, &be, &ga);
-#ifdef JAC_PROBE
-          long long cm;
-          asm volatile("mov.u64 %0, %%clock64;" : "=l"(cm) : "d"(al), "d"(be), "d"(ga) : "memory");
-#endif
-          double c = 1.0, sn = 0.0;
-          const bool rot = rotation(al, be, ga, tol2, &c, &sn);
-#ifdef JAC_PROBE
-          long long cr;
-          asm volatile("mov.u64 %0, %%clock64;" : "=l"(cr) : "d"(c), "d"(sn) : "memory");
-          pacc[6] += cm - c0;
-          pacc[7] += cr - cm;
-#endif
-          const unsigned m2 = __ballot_sync(0xffffffffu, rot) & ((1u << JW) - 1);
-          if (lane < JW) CS[(k + 1) & 1][lane] = make_double2(c, sn);
+          rotate_next(la[(u + 1) * JW + (lane & (JW - 1))], gc, tol2, &cK, &sK, &rK, &dX, &dY);
+          const unsigned m2 = __ballot_sync(0xffffffffu, rK) & ((1u << JW) - 1);
+          if (lane < JW) CS[(k + 1) & 1][lane] = make_double2(cK, sK);
           if (lane == 0) s_mask[(k + 1) & 1] = m2;
         }
 #ifdef JAC_PROBE

@@ -44,7 +44,6 @@ int main(int argc, char** argv) {
     cudaMemcpyFromSymbol(p2, jac::g_probe2, sizeof(p2));
     printf("  sub-round (%llu): worker work %.0f + wait %.0f clk; rotation warp work %.0f + wait %.0f clk\n", p2[2],
            (double)p2[0] / p2[2], (double)p2[1] / p2[2], (double)p2[3] / p2[5], (double)p2[4] / p2[5]);
-    printf("  rotation warp: look-ahead entries %.0f clk, rotation %.0f clk\n", (double)p2[6] / p2[5], (double)p2[7] / p2[5]);
     printf("  SM clock over the rounds kernel: %.0f MHz\n", 1e3 * pr[7] / tot);
     for (int k = 0; k < 7; ++k)
       printf("  %-34s %8.1f us  %5.1f%%\n", names[k], pr[k] / 1e3, 100.0 * pr[k] / tot);
