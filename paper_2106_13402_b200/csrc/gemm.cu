@@ -75,6 +75,12 @@ struct Args {
   int wstore;  // HASC: per-warp TMA stores of the C tile (tmCw, 16 x 32 boxes)
 };
 
+#ifdef GEMM_PROBE
+// tools/gemm_probe.cu: per-phase clock64 cycles of warps 0 and 1 of CTA 0
+// [w][0] tile-start wait (first stage), [1] main loop, [2] of which
+// full-barrier waits, [3] epilogue, [4] tiles
+__device__ unsigned long long g_gprobe[2][8];
+#endif
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -199,16 +205,21 @@ __global__ void __launch_bounds__(THREADS, 1)
     const TileCoord c = tile_of(p, t);
     return (c.mc / BK) * BK >= min(ktot, (c.z + 1) * p.k_split);
   };
+  int nt_pre = -1;  // prefetched scheduler ticket (thread 0)
   auto next_tile = [&](int prev) -> int {
     if (!p.sched) {
       int t = prev < 0 ? (int)blockIdx.x : prev + (int)gridDim.x;
       while (t < p.tiles && empty_unit(t)) t += (int)gridDim.x;
       return t < p.tiles ? t : -1;
     }
+    // the ticket taken when this CTA started producing its current tile
+    // (nt_pre) hides the atomic's round trip from the TMA producer
+    int t = nt_pre >= 0 ? nt_pre : atomicAdd(p.sched, 1);
+    nt_pre = -1;
     while (true) {
-      const int t = atomicAdd(p.sched, 1);
       if (t >= p.tiles) break;
       if (!empty_unit(t)) return t;
+      t = atomicAdd(p.sched, 1);
     }
     if (atomicAdd(p.sched + 1, 1) == (int)gridDim.x - 1) {
       atomicExch(p.sched, 0);
@@ -245,7 +256,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int s = (int)(pg % STAGES);
     if (pg >= STAGES) mbar_wait(empty0 + 8 * s, (uint32_t)(((pg / STAGES) & 1) ^ 1));
     const uint32_t fb = full0 + 8 * s;
-    if (pit == 0) tq[(pseq++) & 7] = ptile;
+    if (pit == 0) {
+      tq[(pseq++) & 7] = ptile;
+      if (p.sched && pnk > 1) nt_pre = atomicAdd(p.sched, 1);  // consumed at this tile's last k-block
+    }
     mbar_arrive_expect_tx(fb, STAGE_BYTES);
     const int k = pkb + pit * BK;  // k' (even)
     const uint32_t dA = smem_u32(sA + s * A_ST), dB = smem_u32(sB + s * B_ST);
@@ -300,12 +314,21 @@ __global__ void __launch_bounds__(THREADS, 1)
   for (int u = 0; u < 4; ++u) bcol[u] = frag_col<TB>(wn, u, fr);
 
   long g = 0;   // global consumed k-block count
+#ifdef GEMM_PROBE
+  long long gp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const bool gprobe = blockIdx.x == 0 && lane == 0 && warp < 2;
+  long long gt0 = clock64();
+#endif
   for (int local = 0;; ++local) {
     // the first stage of the tile publishes its id (or the -1 sentinel)
     if (threadIdx.x == 0 && pg < g + STAGES) produce_one();
     __syncwarp();
     mbar_wait(full0 + 8 * (int)(g % STAGES), (uint32_t)((g / STAGES) & 1));
     const int tile = tq[local & 7];
+#ifdef GEMM_PROBE
+    long long gt1 = clock64();
+    gp[0] += gt1 - gt0;
+#endif
     if (tile < 0) break;
     const TileCoord tc = tile_of(p, tile);
     const int nk = nk_of(tc);
@@ -320,7 +343,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (threadIdx.x == 0 && it > 0 && pg < g + STAGES) produce_one();
       __syncwarp();
       const int s = (int)(g % STAGES);
+#ifdef GEMM_PROBE
+      const long long gw0 = clock64();
+#endif
       mbar_wait(full0 + 8 * s, (uint32_t)((g / STAGES) & 1));
+#ifdef GEMM_PROBE
+      gp[2] += clock64() - gw0;
+#endif
       const double* a = sA + s * A_ST;
       const double* b = sB + s * B_ST;
 #pragma unroll
@@ -347,6 +376,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 
     // ---------------- epilogue ----------------
+#ifdef GEMM_PROBE
+    {
+      const long long gt2 = clock64();
+      gp[1] += gt2 - gt1;
+      gt1 = gt2;
+      gp[4] += 1;
+    }
+#endif
     const int m0 = tc.mc - (TA ? 0 : p.a_sh), n0 = tc.nc - (TB ? p.b_sh : 0);
     if (!HASC && p.flags) {
       // fused split-K (no C tile prefetch: splits > 1 never has HASC)
@@ -405,6 +442,52 @@ __global__ void __launch_bounds__(THREADS, 1)
     // tile containing the last row of an odd-M matrix keeps the direct stores.
     const bool tstore = HASC && p.c_sh == 0 && !w && m0 >= 0 && n0 >= 0 &&
                         ((p.M & 1) == 0 || m0 + BM <= p.M);
+    // Fast paths (the common case): the smem C tile, or a direct store of an
+    // interior tile.  Per fragment row t the eight sC values are gathered
+    // before any is written back (stores cannot alias the later loads, so
+    // the LDS issue back to back instead of one LDS -> DFMA -> STS round
+    // trip per element), and interior stores go through eight precomputed
+    // column pointers with compile-time row offsets (no bounds or address
+    // arithmetic per element).  tools/gemm_probe.cu: the epilogue took
+    // ~7000 of ~80000 cycles per K = 256 tile.
+    const bool interior = !w && m0 >= 0 && n0 >= 0 && m0 + BM <= p.M && n0 + BN <= p.N;
+    if (HASC && tstore) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int ml = frag_row<TA>(wm, t, fr);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // four values at a time (register pressure)
+          double* cs[4];
+          double cv[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            cs[k] = &sC[swz((ml >> 4) * BN + frag_col<TB>(wn, 2 * h + (k >> 1), 2 * fk + (k & 1)), ml & 15)];
+          if (p.beta != 0.0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) cv[k] = *cs[k];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) *cs[k] = fma(p.beta, cv[k], p.alpha * acc[t][2 * h + (k >> 1)][k & 1]);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) *cs[k] = p.alpha * acc[t][2 * h + (k >> 1)][k & 1];
+          }
+        }
+      }
+    } else if (!HASC && interior) {
+      double* cp[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        cp[k] = p.C + m0 + (long)(n0 + frag_col<TB>(wn, k >> 1, 2 * fk + (k & 1))) * p.ldc;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int ml = frag_row<TA>(wm, t, fr);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const double v = p.alpha * acc[t][k >> 1][k & 1];
+          cp[k][ml] = (p.beta == 0.0) ? v : fma(p.beta, cp[k][ml], v);
+        }
+      }
+    } else {
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
       const int ml = frag_row<TA>(wm, t, fr);
@@ -420,16 +503,13 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (HASC) {
             double* cs = &sC[swz((ml >> 4) * BN + nl, ml & 15)];
             if (p.beta != 0.0) v = fma(p.beta, *cs, v);
-            if (tstore) {
-              *cs = v;
-              continue;
-            }
           }
           if (mok && n >= 0 && n < p.N) {
             if (w) w[m + (size_t)n * p.M] = acc[t][u][j];
             else p.C[m + (long)n * p.ldc] = v;
           }
         }
+    }
     }
     if (HASC && p.wstore) {
       // per-warp epilogue: each warp stores its own 64 x 32 sub-tile with
@@ -471,7 +551,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (nxt >= 0 && p.beta != 0.0) load_c(nxt);
       }
     }
+#ifdef GEMM_PROBE
+    gt0 = clock64();
+    gp[3] += gt0 - gt1;
+#endif
   }
+#ifdef GEMM_PROBE
+  if (gprobe)
+    for (int i = 0; i < 8; ++i) g_gprobe[warp][i] += gp[i];
+#endif
   if (HASC && (threadIdx.x == 0 || (p.wstore && lane == 0))) bulk_wait0();
 }
 
