@@ -42,9 +42,9 @@ FP64_PEAK_TFLOPS = 37.1   # measured DMMA m8n8k4 peak on this pool's B200 (profi
 # DRAM traffic of the representative WY-update launch (NT 16384x16384x256,
 # beta=1), one `ncu --set full` capture: read + write bytes per launch vs the
 # algorithmic bytes (A, B 32 MiB each + C read and written, 2 GiB each).
-GEMM_TRAFFIC = {"bytes": 2.821095e9 + 2.106140e9, "algorithmic_bytes": 2 * 8 * 16384 * 256 + 2 * 8 * 16384 ** 2,
+GEMM_TRAFFIC = {"bytes": 2.811756e9 + 2.102741e9, "algorithmic_bytes": 2 * 8 * 16384 * 256 + 2 * 8 * 16384 ** 2,
                 "launch": "dgemm NT M=N=16384 K=256 beta=1 (compact-WY trailing update)",
-                "source": "profiles/r01_ncu_gemm_nt_16384x16384x256_v4.txt"}
+                "source": "profiles/r02_ncu_gemm_nt_16384x16384x256_epilogue.txt"}
 FP64_PEAK_SRC = "measured: tools/fp64_peak.cu DMMA m8n8k4, 148 SMs @1965 MHz (profiles/fp64_peak_r01.json)"
 # dense TF32 tcgen05 peak (M=128, N=128 - K10's MMA shape), measured by
 # tools/tf32_peak.cu (profiles/tf32_peak_r02.json); 3xTF32 does 3 MMAs per
