@@ -96,7 +96,9 @@ int utv_dgeqrf_rows_max(void);
  * original index of column k (0-based, the reference's `perm`).  Greedy
  * largest-norm pivoting with the reference's 1e-12 tie window (leftmost),
  * skip rule and norm downdate/recompute.  A is overwritten (working storage).
- * m, n <= utv_dgeqp3_max_dim(). */
+ * Any m, n: beyond 16384 rows or columns the kernel keeps its per-CTA
+ * reflector and permutation in the workspace (utv_dgeqp3_max_dim() now
+ * returns INT_MAX; kept for callers that probed the old limit). */
 size_t utv_dgeqp3_bufsize(int m, int n);
 int utv_dgeqp3_max_dim(void);
 int utv_dgeqp3_f64(int m, int n, double* A, long lda, double* R, long ldr, double* Y, long ldy,

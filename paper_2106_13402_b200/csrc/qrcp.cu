@@ -38,6 +38,10 @@ namespace pqp {
 constexpr int THREADS = 256;
 constexpr int NW = THREADS / 32;
 constexpr int MAXDIM = 16384;  // v (m doubles) + perm (n ints) + flags fit one CTA's smem
+// Beyond MAXDIM rows or columns the same kernel runs with the per-CTA
+// reflector, permutation and flags in global memory (L2) and the column
+// update in two strided passes instead of registers (BIG); the per-thread
+// summation order is the same, so results are bitwise identical.
 constexpr double EPS = 2.220446049250313e-16;  // matrix.py:13
 constexpr double TIE = 1e-12;                   // qr.py:148 _PIVOT_TIE_RTOL
 
@@ -55,6 +59,9 @@ struct Args {
   const double* fro2;
   int m, n, r;
   unsigned* ctr;
+  double* vbig;          // BIG: [G][m] reflector copies
+  int* pbig;             // BIG: [G][n] permutation copies
+  unsigned char* dbig;   // BIG: [G][n] pivoted flags
 };
 
 __host__ __device__ inline size_t smem_bytes(int m, int n) {
@@ -109,15 +116,15 @@ __device__ __forceinline__ int block_min_int(int x, int* buf) {
   return s;
 }
 
-template <int RPT>
+template <int RPT, bool BIG>
 __global__ void __launch_bounds__(THREADS, 1) qrcp_kernel(Args a) {
   extern __shared__ double sm[];
-  double* v = sm;                          // [m] reflector of the current column
-  double* red = v + a.m;                   // [4][4*NW] reduction slots
-  int* perm_s = (int*)(red + 16 * NW);     // [n] logical -> physical column
-  unsigned char* done_s = (unsigned char*)(perm_s + a.n);  // [n] physical column pivoted
-
   const int t = threadIdx.x, g = blockIdx.x, G = gridDim.x;
+  double* v = BIG ? a.vbig + (size_t)g * a.m : sm;        // [m] reflector of the current column
+  double* red = BIG ? sm : v + a.m;                        // [4][4*NW] reduction slots
+  int* perm_s = BIG ? a.pbig + (size_t)g * a.n : (int*)(red + 16 * NW);  // [n] logical -> physical
+  unsigned char* done_s = BIG ? a.dbig + (size_t)g * a.n : (unsigned char*)(perm_s + a.n);  // [n] pivoted
+
   const int m = a.m, n = a.n;
   const double thresh = EPS * sqrt(*a.fro2);  // qr.py:162 (eps * ||A||_F)
   for (int k = t; k < n; k += THREADS) {
@@ -203,6 +210,25 @@ __global__ void __launch_bounds__(THREADS, 1) qrcp_kernel(Args a) {
       // every thread derives the new row-j entry itself (v[0] = 1, so it is
       // fma(-1, w, A[j,c]) exactly as thread 0 stores it): no extra barrier
       double rj = col[0];
+      if (BIG) {
+        if (!skip) {
+          double d = 0.0;
+          for (int i = t; i < nr; i += THREADS) d = fma(v[i], col[i], d);
+          const double w = tau * block_sum(d, rbuf());
+          for (int i = t; i < nr; i += THREADS) col[i] = fma(-v[i], w, col[i]);
+          rj = fma(-1.0, w, rj);
+        }
+        double nn = fmax(__ldcg(ncur + c) - rj * rj, 0.0);
+        if (nn <= EPS * a.ref[c]) {
+          double s = 0.0;
+          for (int i = t; i < nr; i += THREADS)
+            if (i >= 1) s = fma(col[i], col[i], s);
+          nn = block_sum(s, rbuf());
+          if (t == 0) a.ref[c] = nn;
+        }
+        if (t == 0) nnxt[c] = nn;
+        continue;
+      }
       if (!skip) {
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
@@ -300,26 +326,33 @@ __global__ void larft_kernel(const double* __restrict__ S, long lds, const doubl
 
 }  // namespace pqp
 
-int qrcp_max_dim() { return pqp::MAXDIM; }
+int qrcp_max_dim() { return INT_MAX; }
+
+static bool qrcp_big(int m, int n) {
+  static const bool forced = getenv("UTV_QRCP_BIG") != nullptr;  // test knob
+  return forced || m > pqp::MAXDIM || n > pqp::MAXDIM;
+}
+
+static size_t qrcp_big_doubles(int m, int n) {
+  // one reflector / permutation / flag copy per CTA (at most one CTA per SM)
+  return (size_t)num_sms() * ((size_t)m + (size_t)(n + 1) / 2 + (size_t)(n + 7) / 8 + 64);
+}
 
 size_t qrcp_ws_doubles(int m, int n) {
   const int r = m < n ? m : n;
   const int nblk = (r + QR_PANEL - 1) / QR_PANEL;
   return 3 * (size_t)n + r + 64 + sumsq_scratch_doubles() + (size_t)nblk * QR_PANEL * QR_PANEL +
-         2 * (size_t)round_up(r, 4) * QR_PANEL + SPLITK_WS + 2048;
+         2 * (size_t)round_up(r, 4) * QR_PANEL + SPLITK_WS + 2048 +
+         (qrcp_big(m, n) ? qrcp_big_doubles(m, n) : 0);
 }
 
-static int g_qrcp_attr[3] = {0, 0, 0};
+static int g_qrcp_attr[4] = {0, 0, 0, 0};
 
 int qrcp(int m, int n, double* A, long lda, double* R, long ldr, double* Y, long ldy, double* T,
          long ldt, int* perm, double* ws, size_t ws_doubles, cudaStream_t st) {
   using namespace pqp;
   if (m < 1) return -1;
   if (n < 1) return -2;
-  if (m > MAXDIM || n > MAXDIM) {
-    fprintf(stderr, "libutvb200: hqrcp %dx%d exceeds the device limit %d\n", m, n, MAXDIM);
-    return -1;
-  }
   if (ws_doubles < qrcp_ws_doubles(m, n)) return UTV_ERR_WORKSPACE;
   const int r = m < n ? m : n;
   Arena ar{(char*)ws, ws_doubles * sizeof(double), 0};
@@ -334,6 +367,17 @@ int qrcp(int m, int n, double* A, long lda, double* R, long ldr, double* Y, long
   const size_t bt_n = 2 * (size_t)round_up(r, 4) * QR_PANEL + SPLITK_WS + 512;
   double* bt = ar.take(bt_n);
   if (!bt) return UTV_ERR_WORKSPACE;
+  const bool big = qrcp_big(m, n);
+  double* vbig = nullptr;
+  int* pbig = nullptr;
+  unsigned char* dbig = nullptr;
+  if (big) {
+    const size_t ns = num_sms();
+    vbig = ar.take(ns * (size_t)m);
+    pbig = (int*)ar.take(ns * (size_t)((n + 1) / 2));
+    dbig = (unsigned char*)ar.take(ns * (size_t)((n + 7) / 8));
+    if (!dbig) return UTV_ERR_WORKSPACE;
+  }
 
   UTV_CHECK(sumsq(A, lda, m, n, fro2, red, st));
   UTV_CHECK(set_zero(Y, ldy, m, r, st));
@@ -347,15 +391,17 @@ int qrcp(int m, int n, double* A, long lda, double* R, long ldr, double* Y, long
   a.A = A; a.lda = lda; a.R = R; a.ldr = ldr; a.Y = Y; a.ldy = ldy;
   a.tau = tau; a.perm = perm; a.nrm = nrm; a.ref = ref; a.fro2 = fro2;
   a.m = m; a.n = n; a.r = r; a.ctr = ctr;
-  const size_t smem = smem_bytes(m, n);
+  a.vbig = vbig; a.pbig = pbig; a.dbig = dbig;
+  const size_t smem = big ? 16 * NW * sizeof(double) : smem_bytes(m, n);
   void* fn;
   int ti;
-  if (m <= 4 * THREADS) { fn = (void*)qrcp_kernel<4>; ti = 0; }
-  else if (m <= 16 * THREADS) { fn = (void*)qrcp_kernel<16>; ti = 1; }
-  else { fn = (void*)qrcp_kernel<64>; ti = 2; }
+  if (big) { fn = (void*)qrcp_kernel<1, true>; ti = 3; }
+  else if (m <= 4 * THREADS) { fn = (void*)qrcp_kernel<4, false>; ti = 0; }
+  else if (m <= 16 * THREADS) { fn = (void*)qrcp_kernel<16, false>; ti = 1; }
+  else { fn = (void*)qrcp_kernel<64, false>; ti = 2; }
   if (!g_qrcp_attr[ti]) {
     UTV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem_bytes(MAXDIM, MAXDIM)));
+                                  big ? (int)smem : (int)smem_bytes(MAXDIM, MAXDIM)));
     g_qrcp_attr[ti] = 1;
   }
   // every co-resident CTA streams its own column: more CTAs per SM hide the
@@ -363,7 +409,7 @@ int qrcp(int m, int n, double* A, long lda, double* R, long ldr, double* Y, long
   int occ = 1;
   UTV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, THREADS, smem));
   if (occ < 1) return UTV_ERR_CUDA;
-  if (getenv("UTV_QRCP_OCC1")) occ = 1;
+  if (getenv("UTV_QRCP_OCC1") || big) occ = 1;  // BIG: one workspace copy per SM
   int G = (n + 3) / 4;
   if (G > occ * num_sms()) G = occ * num_sms();
   if (G < 1) G = 1;

@@ -93,8 +93,8 @@ def hqrcp(a):
     """Column-pivoted Householder QR (greedy largest-norm pivoting) — the
     paper's comparator, qr.py:152-204, as one persistent cooperative kernel
     (csrc/qrcp.cu).  Same pivots (1e-12 tie window, leftmost), skip rule and
-    norm downdate/recompute as the reference; any m x n up to the device
-    limit (utv_dgeqp3_max_dim, 16384 per side)."""
+    norm downdate/recompute as the reference; any m x n (beyond 16384 rows or
+    columns the kernel keeps its per-CTA reflector in global memory)."""
     a = check_matrix(a)
     m, n = a.shape
     lim = dv.geqp3_max_dim()

@@ -111,7 +111,44 @@ def test_hqrcp_invariants_4096():
     assert (d[1:] <= d[:-1] * (1 + 1e-10)).all()
 
 
-def test_hqrcp_device_limit_raises():
+@pytest.mark.parametrize("m,n", [(16500, 48), (64, 16500)])
+def test_hqrcp_beyond_the_register_tiles(m, n):
+    """More than 16384 rows or columns: the kernel keeps the per-CTA
+    reflector / permutation in global memory (qr.py:152-204 has no limit)."""
     import paper_2106_13402_b200 as pk
-    with pytest.raises(pk.DimensionError):
-        pk.hqrcp(np.ones((16385, 1)))
+    rng = np.random.default_rng(m + n)
+    k = min(m, n)
+    a = rng.standard_normal((m, n)) * np.exp(-np.arange(n) / (k / 4.0))[None, :]
+    a = a[:, rng.permutation(n)]
+    y, t, r, perm = orc.hqrcp(a)
+    f = pk.hqrcp(a)
+    assert np.array_equal(f.perm[:k], perm[:k])
+    scale = max(1.0, np.abs(r).max())
+    assert np.abs(f.R[:, :k] - r[:, :k]).max() <= 1e-11 * scale
+    assert np.abs(f.q.Y - y).max() <= 1e-10
+
+
+def test_hqrcp_global_variant_is_bitwise_the_register_variant(tmp_path):
+    """UTV_QRCP_BIG=1 forces the global-memory variant at a size the
+    register tiling also covers: same per-thread summation order, so the
+    factors are bitwise equal."""
+    import os
+    import subprocess
+    import sys
+
+    import paper_2106_13402_b200 as pk
+    rng = np.random.default_rng(11)
+    a = rng.standard_normal((1500, 700)) * np.exp(-np.arange(700) / 90.0)[None, :]
+    np.save(tmp_path / "a.npy", a)
+    f = pk.hqrcp(a)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); import paper_2106_13402_b200 as pk; "
+            "f = pk.hqrcp(np.load(%r)); np.savez(%r, R=f.R, Y=f.q.Y, T=f.q.Twy, p=f.perm)"
+            % (root, str(tmp_path / "a.npy"), str(tmp_path / "big.npz")))
+    env = dict(os.environ, UTV_QRCP_BIG="1")
+    subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=600)
+    z = np.load(tmp_path / "big.npz")
+    assert np.array_equal(z["p"], f.perm)
+    assert np.array_equal(z["R"], f.R)
+    assert np.array_equal(z["Y"], f.q.Y)
+    assert np.array_equal(z["T"], f.q.Twy)

@@ -32,7 +32,7 @@ def wrap(obj, name, label):
 
 wrap(powerurv, "dfrom_numpy", "H2D A")
 wrap(powerurv, "raise_if_nonfinite", "finite")
-wrap(dv.PowerUrvRun, "run_yhat", "launch driver")
+wrap(dv.PowerUrvRun, "run_cols", "launch driver")
 wrap(_lib.AsyncD2H, "finish", "D2H finish")
 
 n, q = 16384, 2
