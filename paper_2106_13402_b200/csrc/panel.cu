@@ -191,8 +191,12 @@ __global__ void __launch_bounds__(THREADS, 1) panel_qr_kernel(Args a) {
       ts_column();  // previous column's triangle entries, hidden behind the barrier
       gwait();
       PROBE(2);
-      {  // every CTA: sum the G records, 4 interleaved groups, all loads in flight, fixed order
-        const int e = t & 63, q0 = t >> 6;
+      // every CTA: sum the G dot records (threads 0..127: 4 interleaved groups,
+      // all loads in flight, fixed order); row J is read from its owner's
+      // record alone (the other records hold zeros there, so this is the
+      // same value the full sum gave) — half the L2 traffic of the exchange
+      if (t < 4 * NB) {
+        const int e = t & (NB - 1), q0 = t / NB;
         double v[PMAX];
 #pragma unroll
         for (int k = 0; k < PMAX; ++k) {
@@ -203,13 +207,13 @@ __global__ void __launch_bounds__(THREADS, 1) panel_qr_kernel(Args a) {
 #pragma unroll
         for (int k = 0; k < PMAX; ++k) s += v[k];
         red[q0 * 2 * NB + e] = s;
+      } else if (t < 5 * NB) {
+        const int e = t - 4 * NB;
+        const int gJ = J / a.rc;  // the CTA whose slab holds row J
+        Rv[e] = (gJ < G) ? __ldcg(&a.part[((size_t)par * G + gJ) * 2 * NB + NB + e]) : 0.0;
       }
       __syncthreads();
-      if (t < 2 * NB) {
-        const double s = (red[t] + red[2 * NB + t]) + (red[4 * NB + t] + red[6 * NB + t]);
-        if (t < NB) Sv[t] = s;
-        else Rv[t - NB] = s;
-      }
+      if (t < NB) Sv[t] = (red[t] + red[2 * NB + t]) + (red[4 * NB + t] + red[6 * NB + t]);
       __syncthreads();
 
       PROBE(3);
