@@ -302,3 +302,32 @@ def test_public_api_concurrent_threads_match_sequential():
         t.join()
     assert np.array_equal(out[0].R, seq[0].R) and np.array_equal(out[0].Vq.Y, seq[0].Vq.Y)
     assert np.array_equal(out[1].T, seq[1].T) and np.array_equal(out[1].U, seq[1].U)
+
+
+def test_power_urv_overlapped_upload_is_bitwise_the_serial_one():
+    """n >= STREAM_MIN_N and >= OVERLAP_A_MIN_BYTES: A goes up block by block
+    under the G draw (powerurv._power_urv_streamed).  Same chunks, same
+    GEMMs: the factors equal the serial-upload path bit for bit, and a
+    non-finite A raises ValueError without advancing the caller's stream."""
+    import paper_2106_13402_b200 as pk
+    from paper_2106_13402_b200 import powerurv
+    n = 3072
+    rng = np.random.default_rng(31)
+    a = np.asfortranarray(rng.standard_normal((n, n)) * np.logspace(0, -6, n)[None, :])
+    assert a.nbytes >= powerurv.OVERLAP_A_MIN_BYTES
+    f = pk.power_urv(a, 1, pk.RngStream(8))
+    old = powerurv.OVERLAP_A_MIN_BYTES
+    powerurv.OVERLAP_A_MIN_BYTES = 1 << 62
+    try:
+        g = pk.power_urv(a, 1, pk.RngStream(8))
+    finally:
+        powerurv.OVERLAP_A_MIN_BYTES = old
+    assert np.array_equal(f.R, g.R)
+    assert np.array_equal(f.Uq.Y, g.Uq.Y) and np.array_equal(f.Uq.Twy, g.Uq.Twy)
+    assert np.array_equal(f.Vq.Y, g.Vq.Y) and np.array_equal(f.Vq.Twy, g.Vq.Twy)
+    bad = a.copy()
+    bad[n - 7, n - 3] = np.inf                # in the last column block
+    s = pk.RngStream(8)
+    with pytest.raises(ValueError):
+        pk.power_urv(bad, 1, s)
+    assert np.array_equal(s.standard_normal(2, 3), pk.RngStream(8).standard_normal(2, 3))

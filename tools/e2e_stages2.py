@@ -38,7 +38,7 @@ wrap(_lib.AsyncD2H, "finish", "D2H finish")
 n, q = 16384, 2
 a = np.asfortranarray(np.random.default_rng(0).standard_normal((n, n)))
 torch.zeros(1, device="cuda")
-for rep in range(3):
+for rep in range(5):
     marks.clear()
     mark("start")
     f = pk.power_urv(a, q, pk.RngStream(2))
