@@ -194,6 +194,17 @@ int utv_randutv_basic_steps_f64(int i0, int i1, int m, int n, int b, int q, doub
                                 double* U, long ldu, double* V, long ldv, const double* G, long ldg,
                                 double* errsq, double* trail2, int* svd_status, void* work,
                                 size_t lwork, void* stream);
+/* The same with the SVD pipeline carried across range boundaries: carry
+ * bit 0 = the previous range (steps [.., i0)) was called with bit 1 and left
+ * step i0-1's b x b SVD in flight; bit 1 = leave step i1-1's SVD in flight
+ * (its rotations of U, V and T columns [(i1-1) b, i1 b) are then applied by
+ * the next range, so only columns < (i1-1) b are final on return).  Same
+ * bits as one utv_randutv_basic_f64 call.  Replaces the per-step loop of
+ * _randutv (randutv.py:110-182) split into host-fed groups. */
+int utv_randutv_basic_steps_carry_f64(int i0, int i1, int carry, int m, int n, int b, int q,
+                                      double* T, long ldt, double* U, long ldu, double* V, long ldv,
+                                      const double* G, long ldg, double* errsq, double* trail2,
+                                      int* svd_status, void* work, size_t lwork, void* stream);
 
 /* One step i (0-based) of blocked randUTV — the host loop of the boosted
  * (Algorithm 2) and partial variants (randutv_boosted / randutv_partial,

@@ -53,6 +53,10 @@ SIGNATURES = {
                                             c_long, c_void_p, c_long, c_void_p, c_long, c_void_p,
                                             c_long, c_void_p, c_void_p, c_void_p, c_void_p,
                                             c_size_t, c_void_p]),
+    "utv_randutv_basic_steps_carry_f64": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+                                                  c_void_p, c_long, c_void_p, c_long, c_void_p, c_long,
+                                                  c_void_p, c_long, c_void_p, c_void_p, c_void_p,
+                                                  c_void_p, c_size_t, c_void_p]),
     "utv_randutv_step_bufsize": (c_size_t, [c_int, c_int, c_int, c_int, c_int]),
     "utv_randutv_step_f64": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p,
                                      c_long, c_void_p, c_long, c_void_p, c_long, c_void_p, c_long,

@@ -12,7 +12,7 @@ int randutv_basic(int m, int n, int b, int q, Mat T, Mat U, Mat V, const double*
 size_t randutv_ws_doubles_p(int m, int n, int b, int p);
 int randutv_basic_range(int i0, int i1, int m, int n, int b, int q, Mat T, Mat U, Mat V,
                         const double* G, long ldg, double* errsq, double* trail2, int* svd_status,
-                        double* ws, size_t ws_doubles, cudaStream_t st);
+                        double* ws, size_t ws_doubles, cudaStream_t st, int carry);
 int randutv_step(int i, int m, int n, int b, int p, int q, bool boosted, Mat T, Mat U, Mat V,
                  const double* G, long ldg, double* errsq, double* trail2, int* svd_status,
                  double* ws, size_t ws_doubles, int* carried, int* is_final, cudaStream_t st);
@@ -152,7 +152,25 @@ int utv_randutv_basic_steps_f64(int i0, int i1, int m, int n, int b, int q, doub
   UTV_DRIVER_GUARD();
   return randutv_basic_range(i0, i1, m, n, b, q, Mat{T, ldt, m, n}, Mat{U, ldu, m, m},
                              Mat{V, ldv, n, n}, G, ldg, errsq, trail2, svd_status, (double*)work,
-                             lwork / sizeof(double), S(stream));
+                             lwork / sizeof(double), S(stream), 0);
+}
+
+int utv_randutv_basic_steps_carry_f64(int i0, int i1, int carry, int m, int n, int b, int q,
+                                      double* T, long ldt, double* U, long ldu, double* V, long ldv,
+                                      const double* G, long ldg, double* errsq, double* trail2,
+                                      int* svd_status, void* work, size_t lwork, void* stream) {
+  if (i0 < 0 || i1 < i0) return -1;
+  if (carry < 0 || carry > 3) return -3;
+  if (m < n || n < 1) return -4;
+  if (b < 1 || b > 1024) return -6;
+  if (q < 0) return -7;
+  if (!ld_ok(ldt, m)) return -9;
+  if (!ld_ok(ldu, m)) return -11;
+  if (!ld_ok(ldv, n)) return -13;
+  UTV_DRIVER_GUARD();
+  return randutv_basic_range(i0, i1, m, n, b, q, Mat{T, ldt, m, n}, Mat{U, ldu, m, m},
+                             Mat{V, ldv, n, n}, G, ldg, errsq, trail2, svd_status, (double*)work,
+                             lwork / sizeof(double), S(stream), carry);
 }
 
 size_t utv_randutv_step_bufsize(int m, int n, int b, int p, int) { return B(randutv_ws_doubles_p(m, n, b, p)); }

@@ -298,20 +298,24 @@ static int side_stream(cudaStream_t* s1, cudaEvent_t* ev, cudaStream_t* s2 = nul
 // as the one-stream step sequence.
 int randutv_basic_range(int i0, int i1, int m, int n, int b, int q, Mat T, Mat U, Mat V,
                         const double* G, long ldg, double* errsq, double* trail2, int* svd_status,
-                        double* ws, size_t ws_doubles, cudaStream_t st);
+                        double* ws, size_t ws_doubles, cudaStream_t st, int carry);
 
 int randutv_basic(int m, int n, int b, int q, Mat T, Mat U, Mat V, const double* G, long ldg,
                   double* errsq, double* trail2, int* svd_status, double* ws, size_t ws_doubles,
                   cudaStream_t st) {
   return randutv_basic_range(0, (n + b - 1) / b, m, n, b, q, T, U, V, G, ldg, errsq, trail2,
-                             svd_status, ws, ws_doubles, st);
+                             svd_status, ws, ws_doubles, st, 0);
 }
 
 // Steps [i0, i1) of the basic loop (G = the block of step i0 at column 0).
 // Lets the host draw the next steps' Gaussian blocks while these run.
+// carry bit 0: the previous range left step i0-1's SVD in flight (its
+// rotations are applied here, where the one-call loop would); bit 1: leave
+// step i1-1's SVD in flight for the next range.  Without the carry, every
+// range boundary drains the SVD pipeline (~3-5 ms per boundary).
 int randutv_basic_range(int i0, int i1, int m, int n, int b, int q, Mat T, Mat U, Mat V,
                         const double* G, long ldg, double* errsq, double* trail2, int* svd_status,
-                        double* ws, size_t ws_doubles, cudaStream_t st) {
+                        double* ws, size_t ws_doubles, cudaStream_t st, int carry) {
   if (m < n) return -1;
   if (b < 1) return -3;
   if (q < 0) return -4;
@@ -338,7 +342,7 @@ int randutv_basic_range(int i0, int i1, int m, int n, int b, int q, Mat T, Mat U
   UTV_CHECK(side_stream(&s1, ev, &s2));
   const int nsteps = (n + b - 1) / b < i1 ? (n + b - 1) / b : i1;
   long gcol = 0;
-  int pending = -1;  // step whose SVD (and side transforms) are in flight
+  int pending = ((carry & 1) && i0 > 0) ? i0 - 1 : -1;  // step whose SVD (and side transforms) are in flight
   auto finish_pending = [&]() -> int {
     if (pending < 0) return UTV_OK;
     UTV_CUDA(cudaStreamWaitEvent(st, ev[1], 0));
@@ -401,7 +405,7 @@ int randutv_basic_range(int i0, int i1, int m, int n, int b, int q, Mat T, Mat U
       UTV_CHECK(larfb('L', true, Yu, Tu, T.sub(lo, lo + b, k, kc - b), w.lfb, w.lfb_n, st));
     }
   }
-  UTV_CHECK(finish_pending());
+  if (!(carry & 2) || pending < 0 || pending + 1 >= (n + b - 1) / b) UTV_CHECK(finish_pending());
   return UTV_OK;
 }
 

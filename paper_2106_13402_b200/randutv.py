@@ -328,13 +328,17 @@ def _randutv_basic_pipelined(a, b, q, rng, record_trailing):
                 ev.record(copy_stream)
             comp.wait_event(ev)
         gptr = G.at(0, int(offs[d0])) if ncol > 0 else G.ptr
-        _lib.check(lib.utv_randutv_basic_steps_f64(
-            j0, j1, m, n, b, q, t_dev.ptr, t_dev.ld, U.ptr, U.ld, V.ptr, V.ld, gptr, G.ld,
+        # the b x b SVD of a group's last step stays in flight into the next
+        # group (its rotations land there), so group boundaries do not drain
+        # the SVD pipeline; only columns < (j1 - 1) b are final on return
+        carry = (1 if gi > 0 else 0) | (2 if j1 < steps else 0)
+        _lib.check(lib.utv_randutv_basic_steps_carry_f64(
+            j0, j1, carry, m, n, b, q, t_dev.ptr, t_dev.ld, U.ptr, U.ld, V.ptr, V.ld, gptr, G.ld,
             run.errsq.data_ptr(), run.trail2.data_ptr() if run.trail2 is not None else None,
             run.status.data_ptr(), run.ws.data_ptr(), run.lw, _lib.stream_ptr()),
-            "utv_randutv_basic_steps_f64")
+            "utv_randutv_basic_steps_carry_f64")
         if contiguous:
-            fin = min(n, j1 * b) if j1 < steps else n
+            fin = min(n, (j1 - 1) * b) if j1 < steps else n
             if fin > done_cols:
                 ev = torch.cuda.Event()
                 ev.record(comp)

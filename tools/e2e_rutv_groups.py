@@ -14,7 +14,7 @@ from paper_2106_13402_b200 import _lib, randutv
 n, b, q = 16384, 256, 2
 a = np.asfortranarray(np.random.default_rng(0).standard_normal((n, n)))
 lib = _lib.load()
-orig = lib.utv_randutv_basic_steps_f64
+orig = lib.utv_randutv_basic_steps_carry_f64
 log = []
 
 
@@ -22,7 +22,7 @@ class Wrap:
     def __getattr__(self, k):
         return getattr(lib, k)
 
-    def utv_randutv_basic_steps_f64(self, *args):
+    def utv_randutv_basic_steps_carry_f64(self, *args):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         h0 = time.perf_counter()
         e0.record()
