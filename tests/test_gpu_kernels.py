@@ -295,3 +295,50 @@ def test_powerurv_progressive_columns_match_the_plain_driver(m, n, q):
         run2.run_cols(a, None, yh)
         torch.cuda.synchronize()
         assert np.abs(run2.R.to_numpy() - ref.R.to_numpy()).max() < 1e-12 * np.abs(ref.R.to_numpy()).max()
+
+
+@pytest.mark.parametrize("groups", [[1, 3, 4, 4], [2, 2, 5], [1] * 12])
+def test_randutv_step_ranges_with_carried_svd_are_bitwise_one_call(groups):
+    """utv_randutv_basic_steps_carry_f64 over host-fed groups (the last
+    step's SVD left in flight into the next group) gives exactly the bits
+    of one utv_randutv_basic_f64 call; columns < (j1-1) b are final when a
+    carrying group returns."""
+    import torch
+
+    import paper_2106_13402_b200.device as dv
+    from paper_2106_13402_b200 import _lib
+    from paper_2106_13402_b200._lib import dempty, deye, dfrom_numpy
+    m, n, b, q = 700, 660, 64, 2
+    steps = -(-n // b)
+    rng = np.random.default_rng(17)
+    a = rng.standard_normal((m, n)) * np.logspace(0, -6, n)[None, :]
+    blocks = [rng.standard_normal((m - i * b, b)) for i in range(steps - 1)]
+    G = dv.stage_randutv_blocks(blocks, b)
+    run = dv.RandUtvRun(m, n, b, q)
+    T1, U1, V1 = dfrom_numpy(a), deye(m), deye(n)
+    run.run(T1, U1, V1, G)
+    ref = [x.to_numpy() for x in (T1, U1, V1)] + [run.errsq.cpu().numpy()]
+    run2 = dv.RandUtvRun(m, n, b, q)
+    T2, U2, V2 = dfrom_numpy(a), deye(m), deye(n)
+    lib = _lib.load()
+    offs = np.concatenate([[0], np.cumsum([m - i * b for i in range(steps - 1)])]).astype(int)
+    j0 = 0
+    for gi, w in enumerate(groups + [steps]):
+        j1 = min(steps, j0 + w)
+        if j0 >= j1:
+            break
+        carry = (1 if gi > 0 else 0) | (2 if j1 < steps else 0)
+        gptr = G.at(0, int(offs[min(j0, steps - 1)]))
+        _lib.check(lib.utv_randutv_basic_steps_carry_f64(
+            j0, j1, carry, m, n, b, q, T2.ptr, T2.ld, U2.ptr, U2.ld, V2.ptr, V2.ld, gptr, G.ld,
+            run2.errsq.data_ptr(), None, run2.status.data_ptr(), run2.ws.data_ptr(), run2.lw,
+            _lib.stream_ptr()), "steps_carry")
+        if j1 < steps:       # the carried step's columns are not final yet, the earlier ones are
+            torch.cuda.synchronize()
+            fin = (j1 - 1) * b
+            assert np.array_equal(U2.to_numpy()[:, :fin], ref[1][:, :fin])
+            assert np.array_equal(V2.to_numpy()[:, :fin], ref[2][:, :fin])
+        j0 = j1
+    got = [x.to_numpy() for x in (T2, U2, V2)] + [run2.errsq.cpu().numpy()]
+    for x, y in zip(got, ref):
+        assert np.array_equal(x, y)
