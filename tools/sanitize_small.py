@@ -21,6 +21,10 @@ if what in ("all", "qr"):
     a = dfrom_numpy(rng.standard_normal((96, 40))); dv.geqrf(a)
 if what in ("all", "svd"):
     dv.gesvj(dfrom_numpy(np.triu(rng.standard_normal((70, 70)))))
+    dv.gesvj(dfrom_numpy(rng.standard_normal((256, 256)) * np.logspace(0, -4, 256)))   # 4-CTA clusters
+    dv.gesvj(dfrom_numpy(rng.standard_normal((20, 20))))
+if what in ("all", "qrcp"):
+    pk.hqrcp(rng.standard_normal((300, 200)))
 if what in ("all", "rutv"):
     a, _ = orc.decay_matrix(200, 1e-5, seed=3)
     pk.randutv_basic(a, 48, 1, pk.RngStream(1), record_trailing=True)
@@ -41,6 +45,12 @@ if what in ("all", "purv_stream"):
     import paper_2106_13402_b200.powerurv as pu
     pu.STREAM_MIN_N = 64
     a, _ = orc.decay_matrix(200, 1e-5, seed=5, m=260)
+    pk.power_urv(a, 1, pk.RngStream(3))
+if what in ("all", "purv_overlap"):
+    import paper_2106_13402_b200.powerurv as pu
+    pu.STREAM_MIN_N = 64
+    pu.OVERLAP_A_MIN_BYTES = 1 << 16
+    a, _ = orc.decay_matrix(200, 1e-5, seed=6, m=260)
     pk.power_urv(a, 1, pk.RngStream(3))
 torch.cuda.synchronize()
 print("done", what)
