@@ -36,6 +36,9 @@ namespace pqr {
 // Diagnostics: build with -DPANEL_PROBE (tools/panel_probe.cu) to accumulate
 // CTA 0's per-phase %globaltimer durations into g_probe.
 #ifdef PANEL_PROBE
+#ifndef PANEL_PROBE_CTA
+#define PANEL_PROBE_CTA 0
+#endif
 __device__ unsigned long long g_probe[16];
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long v;
@@ -43,7 +46,7 @@ __device__ __forceinline__ unsigned long long gtime() {
   return v;
 }
 #define PROBE(k)                                   \
-  if (blockIdx.x == 0 && threadIdx.x == 0) {       \
+  if (blockIdx.x == PANEL_PROBE_CTA && threadIdx.x == 0) { \
     const unsigned long long now_ = gtime();       \
     g_probe[k] += now_ - probe_last;               \
     probe_last = now_;                             \
