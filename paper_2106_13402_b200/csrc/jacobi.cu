@@ -676,8 +676,6 @@ int gesvj_ex(Mat A, double* sigma, Mat U, Mat V, double* ws, size_t ws_doubles, 
   a.rot = (int*)ctl;
   a.ctr = (unsigned*)(ctl + jac::MAX_SWEEPS);
   a.status = status_dev;
-  const int R = ne / C;
-  const size_t smem = ((size_t)2 * R * jac::GP + jac::JC * jac::JC + 3 * jac::JC * jac::GP) * sizeof(double);
   if (!g_jac_attr) {
     UTV_CUDA(cudaFuncSetAttribute(jac::jacobi_rounds_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -685,24 +683,40 @@ int gesvj_ex(Mat A, double* sigma, Mat U, Mat V, double* ws, size_t ws_doubles, 
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     g_jac_attr = true;
   }
-  if (smem > 200 * 1024) return -1;
   {
     ProfScope ps(PROF_JACOBI, 0.0, 0.0, st);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((nblk / 2) * C);
-    cfg.blockDim = dim3(jac::JTHREADS);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = C;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    at[1].id = cudaLaunchAttributeCooperative;
-    at[1].val.cooperative = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 2;
-    UTV_CUDA(cudaLaunchKernelEx(&cfg, jac::jacobi_rounds_kernel, a));
+    // a cooperative cluster grid the device cannot hold co-resident (fewer
+    // SMs, MIG) falls back to smaller clusters: same rotations, same bits
+    // up to the Gram partial-sum grouping
+    for (int c = C;; c >>= 1) {
+      const int nec = (int)round_up(n, 2 * c);
+      const int R = nec / c;
+      const size_t smem =
+          ((size_t)2 * R * jac::GP + jac::JC * jac::JC + 3 * jac::JC * jac::GP) * sizeof(double);
+      if (smem > 200 * 1024) return -1;
+      a.ne = nec;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((nblk / 2) * c);
+      cfg.blockDim = dim3(jac::JTHREADS);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute at[2];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = c;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      at[1].id = cudaLaunchAttributeCooperative;
+      at[1].val.cooperative = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 2;
+      const cudaError_t e = cudaLaunchKernelEx(&cfg, jac::jacobi_rounds_kernel, a);
+      if (e == cudaSuccess) break;
+      if (c == 1 || (e != cudaErrorCooperativeLaunchTooLarge)) {
+        fprintf(stderr, "libutvb200: jacobi_rounds_kernel launch failed: %s\n", cudaGetErrorString(e));
+        return UTV_ERR_CUDA;
+      }
+      (void)cudaGetLastError();  // clear the launch error, retry with half the cluster
+    }
   }
   const size_t smem2 = (size_t)4 * (n + 2) * sizeof(double);
   ProfScope ps2(PROF_JFINISH, 0.0, 0.0, st);
