@@ -51,6 +51,13 @@ def test_argument_validation_without_device():
     # both event arguments of the _ev entry are optional
     assert lib.utv_powerurv_f64_ev(4, 4, -1, 0, 4, 0, 4, 0, 4, 0, 4, 0, 4, 0, 4, 0, 4, 0, 0, 0,
                                    None, None) == -3
+    # step ranges with the carried SVD: range order, carry flags, argument indices
+    st = [0, 2, 0, 8, 8, 4, 1, 0, 8, 0, 8, 0, 8, 0, 8, 0, 0, 0, 0, 0, 0]
+    assert lib.utv_randutv_basic_steps_carry_f64(*([2, 1] + st[2:])) == -1           # i1 < i0
+    assert lib.utv_randutv_basic_steps_carry_f64(*(st[:2] + [4] + st[3:])) == -3     # carry bits
+    assert lib.utv_randutv_basic_steps_carry_f64(*(st[:3] + [4, 8] + st[5:])) == -4  # m < n
+    assert lib.utv_randutv_basic_steps_carry_f64(*(st[:5] + [0] + st[6:])) == -6     # b < 1
+    assert lib.utv_randutv_basic_steps_carry_f64(*(st[:8] + [7] + st[9:])) == -9     # ldt < m
 
 
 def test_flop_model_matches_survey():
