@@ -316,19 +316,28 @@ __global__ void __launch_bounds__(JTHREADS, 1) jacobi_rounds_kernel(Args a) {
       }
       __syncthreads();
       JPROBE(0);
-      // 2. partial Gram: warp w rows w and w + JW, lane j column j
+      // 2. partial Gram A_r^T A_r on the FP64 tensor cores (DMMA 8x8x4):
+      //    warp w owns the 8x8 output tile (w / 4, w % 4), K = R slice rows
       if (!rwarp) {
-        double g0 = 0.0, g1 = 0.0, h0 = 0.0, h1 = 0.0;
-        int k = 0;
-        for (; k + 1 < R; k += 2) {
-          const double v = As[k * GP + lane], w = As[(k + 1) * GP + lane];
-          g0 = fma(As[k * GP + warp], v, g0);
-          g1 = fma(As[k * GP + warp + JW], v, g1);
-          h0 = fma(As[(k + 1) * GP + warp], w, h0);
-          h1 = fma(As[(k + 1) * GP + warp + JW], w, h1);
+        const int g = lane >> 2, tq = lane & 3;
+        const int i0 = 8 * (warp >> 2), j0 = 8 * (warp & 3);
+        // four independent accumulator chains over the k-steps (R is a
+        // multiple of 8: k0 and k0 + 4 of every 8-row tile), summed at the end
+        double c[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+        int k0 = 0;
+        for (; k0 + 16 <= R; k0 += 16) {
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const int kk = k0 + 4 * h + tq;
+            dmma884(c[h][0], c[h][1], As[kk * GP + i0 + g], As[kk * GP + j0 + g]);  // (A^T)[i][k] A[k][j]
+          }
         }
-        Gp[warp * JC + lane] = g0 + h0;
-        Gp[(warp + JW) * JC + lane] = g1 + h1;
+        for (; k0 < R; k0 += 4) {
+          const int kk = k0 + tq;
+          dmma884(c[0][0], c[0][1], As[kk * GP + i0 + g], As[kk * GP + j0 + g]);
+        }
+        Gp[(i0 + g) * JC + j0 + 2 * tq] = (c[0][0] + c[1][0]) + (c[2][0] + c[3][0]);
+        Gp[(i0 + g) * JC + j0 + 2 * tq + 1] = (c[0][1] + c[1][1]) + (c[2][1] + c[3][1]);
       }
       JPROBE(1);
       if (C > 1) cluster_sync_all();
@@ -427,19 +436,31 @@ __global__ void __launch_bounds__(JTHREADS, 1) jacobi_rounds_kernel(Args a) {
       JPROBE(3);
       // 4. A_r <- A_r J, V_r <- V_r J (warp w rows w, w + JW, ...), store
       if (nrot) {
-        if (!rwarp)
-          for (int k = warp; k < R; k += JW) {
-            double oa = 0.0, ov = 0.0;
-#pragma unroll 8
-            for (int l = 0; l < JC; ++l) {
-              const double jl = J[l * GP + lane];
-              oa = fma(As[k * GP + l], jl, oa);
-              ov = fma(Vs[k * GP + l], jl, ov);
+        // DMMA 8x8x4: job = (8-row tile, matrix A or V); each warp computes
+        // its tile's 8 x 32 block of M_r J and writes it back over its own rows
+        if (!rwarp) {
+          const int g = lane >> 2, tq = lane & 3;
+          const int jobs = 2 * (R / 8);
+          for (int job = warp; job < jobs; job += JW) {
+            double* M = (job & 1) ? Vs : As;
+            const int r0 = 8 * (job >> 1);
+            double acc[4][2];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[c][0] = acc[c][1] = 0.0;
+#pragma unroll
+            for (int l0 = 0; l0 < JC; l0 += 4) {
+              const double av = M[(r0 + g) * GP + l0 + tq];
+#pragma unroll
+              for (int c = 0; c < 4; ++c) dmma884(acc[c][0], acc[c][1], av, J[(l0 + tq) * GP + 8 * c + g]);
             }
             __syncwarp();
-            As[k * GP + lane] = oa;
-            Vs[k * GP + lane] = ov;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              M[(r0 + g) * GP + 8 * c + 2 * tq] = acc[c][0];
+              M[(r0 + g) * GP + 8 * c + 2 * tq + 1] = acc[c][1];
+            }
           }
+        }
         __syncthreads();
         JPROBE(4);
         for (int idx = threadIdx.x; idx < JC * R2; idx += JTHREADS) {
@@ -614,11 +635,11 @@ static inline int jac_cluster(int n) {
   const int pairs = jac_blocks(n) / 2;
   int c = forced == 1 || forced == 2 || forced == 4 || forced == 8 ? forced : (n >= 128 ? 4 : (n >= 32 ? 2 : 1));
   while (c > 1 && pairs * c > 148) c >>= 1;
-  while (c < 8 && (round_up(n, 2 * c) / c) > 256) c <<= 1;
+  while (c < 8 && (round_up(n, 8 * c) / c) > 256) c <<= 1;
   return c;
 }
 
-static inline long jac_ld(int n) { return round_up(n, 16); }
+static inline long jac_ld(int n) { return round_up(n, 64); }  // >= round_up(n, 8 C), C <= 8
 
 size_t gesvj_ws_doubles(int n) {
   const long ld = jac_ld(n);
@@ -649,9 +670,9 @@ int gesvj_ex(Mat A, double* sigma, Mat U, Mat V, double* ws, size_t ws_doubles, 
   double* ctl = ar.take(jac::MAX_SWEEPS + 64);
   double* scratch = ar.take(1024);
   if (!scratch) return UTV_ERR_WORKSPACE;
-  // rows are padded to a multiple of 2C (16-byte vector moves, equal slices);
-  // padding is zero
-  const int ne = (int)round_up(n, 2 * C);
+  // rows are padded to a multiple of 8C (equal slices of whole 8-row DMMA
+  // tiles); padding is zero
+  const int ne = (int)round_up(n, 8 * C);
   // The rounds run on A^T (UTV_JAC_TRANSPOSE, default on): for the graded
   // upper-triangular blocks randUTV hands in, the columns of R^T start much
   // closer to orthogonal, so far fewer rotations fire (256^2 Gaussian-decay
@@ -689,7 +710,7 @@ int gesvj_ex(Mat A, double* sigma, Mat U, Mat V, double* ws, size_t ws_doubles, 
     // SMs, MIG) falls back to smaller clusters: same rotations, same bits
     // up to the Gram partial-sum grouping
     for (int c = C;; c >>= 1) {
-      const int nec = (int)round_up(n, 2 * c);
+      const int nec = (int)round_up(n, 8 * c);  // 8-row tiles per slice (DMMA)
       const int R = nec / c;
       const size_t smem =
           ((size_t)2 * R * jac::GP + jac::JC * jac::JC + 3 * jac::JC * jac::GP) * sizeof(double);
