@@ -13,12 +13,14 @@
 // 2P blocks of 16; every round of the circle-method tournament a thread-block
 // cluster of C CTAs owns one block pair, CTA r holding a slice of R = ne / C
 // rows of the pair's 32 columns of A and V in shared memory.  The cluster
-// forms the pair's 32 x 32 Gram matrix (partials summed over DSMEM), runs the
-// rotation sub-rounds on it (one warp per rotation, no dot products), and
-// applies the accumulated 32 x 32 rotation to its A and V rows; A and V live
-// in an L2-resident workspace between rounds (grid barrier).  The rounds were
-// smem-bandwidth bound when every rotation re-read and rewrote both columns
-// (tools/jacobi_probe.cu: 1.76 us per sub-round at n = 256).  A second kernel
+// forms the pair's 32 x 32 Gram matrix (DMMA partials summed over DSMEM),
+// runs the rotation sub-rounds on it (a pipelined rotation warp computes the
+// next sub-round's rotations while 16 warps apply the current one to G and
+// to the accumulated rotation J; no dot products), and applies J to its A and
+// V rows (DMMA); A and V live in an L2-resident workspace between rounds
+// (grid barrier).  The rounds were smem-bandwidth bound when every rotation
+// re-read and rewrote both columns (tools/jacobi_probe.cu: 1.76 us per
+// sub-round at n = 256, now ~0.55 us).  A second kernel
 // forms sigma, sorts, normalises U = A V / sigma, completes null columns of U
 // by CGS2 against the standard basis, and applies the sign rule.
 #include "common.cuh"
